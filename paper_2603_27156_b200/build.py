@@ -1,0 +1,48 @@
+"""In-tree build of the sm_100a CUDA library (libgsrcuda.so).
+
+nvcc cross-compiles for sm_100a without a GPU. Objects are rebuilt only when
+their sources change, so the driver's build() check stays fast.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libgsrcuda.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+SOURCES = ["kernels.cu", "capi.cu"]
+HEADERS = ["kernels.cuh", os.path.join(ROOT, "include", "gsr_cuda.h")]
+
+
+def _mtime(p):
+    return os.path.getmtime(p) if os.path.exists(p) else 0.0
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(os.path.join(CSRC, "_obj"), exist_ok=True)
+    hdr_t = max(_mtime(os.path.join(CSRC, h)) if not os.path.isabs(h) else _mtime(h) for h in HEADERS)
+    objs = []
+    for src in SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(CSRC, "_obj", src.replace(".cu", ".o"))
+        objs.append(o)
+        if _mtime(o) < max(_mtime(s), hdr_t):
+            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.check_call(cmd)
+    if _mtime(LIB) < max(_mtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))

@@ -1,0 +1,1088 @@
+// C-ABI implementation (include/gsr_cuda.h): context, device arena, graph /
+// model / data upload, and the host-side orchestration of the GSR-GNN
+// training step on one stream (optionally replayed from a CUDA graph).
+//
+// Layer orchestration follows the reference spec:
+//   GSRC  — Eq. 6-7 grouped reversible layer (PAPER.md:275-276,
+//           SPEC.md:316-342) with GS-sparse blocks f_i(u) = Â·scatter(GS_k(u))·W_i
+//           + b_i (gsr_forward_block SPEC.md:253-256): forward keeps only the
+//           final activation; backward reconstructs each layer input by
+//           inverse recomputation and back-propagates the exact gradient.
+//   ALG12 — Algorithms 1-2 verbatim
+//           with the per-layer index/value caches the paper keeps (O(LNk)).
+//   REV   — rev-baseline dense blocks.
+// Every kernel launch goes through launch_tile / launch_gs / the small
+// kernels in kernels.cu; there is no host or CPU fallback for any of them.
+#include "../../include/gsr_cuda.h"
+#include "kernels.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace gsrk;
+
+namespace {
+
+struct Fail : std::runtime_error {
+    int code;
+    Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, int line) {
+    const int code = (e == cudaErrorMemoryAllocation) ? GSRC_ERR_RESOURCE : GSRC_ERR_INTERNAL;
+    throw Fail(code, std::string("CUDA error '") + cudaGetErrorString(e) + "' at capi.cu:" + std::to_string(line) + " (" + what + ")");
+}
+#define CK(x)                                                 \
+    do {                                                      \
+        cudaError_t e_ = (x);                                 \
+        if (e_ != cudaSuccess) throw_cuda(e_, #x, __LINE__);  \
+    } while (0)
+
+[[noreturn]] void cfg_err(const std::string& m) { throw Fail(GSRC_ERR_CONFIG, m); }
+[[noreturn]] void seq_err(const std::string& m) { throw Fail(GSRC_ERR_SEQUENCING, m); }
+
+// Single contiguous device arena (SPEC mem-arena; north_star
+// "one contiguous activation arena"). Buffers are carved at plan time; the
+// steady-state step performs zero allocations.
+struct Arena {
+    char* base = nullptr;
+    size_t reserved = 0, used = 0, peak_active = 0, peak_reserved = 0;
+    uint64_t alloc_count = 0, reuse_count = 0, release_count = 0;
+    int leases = 0;
+
+    void plan(size_t bytes) {
+        release_all();
+        if (bytes > reserved) {
+            if (base) { cudaFree(base); base = nullptr; reserved = 0; }
+            cudaError_t e = cudaMalloc(&base, bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw Fail(GSRC_ERR_RESOURCE, "arena: cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e) +
+                                                  " [reserved=" + std::to_string(reserved) + " active=" + std::to_string(used) + "]");
+            }
+            reserved = bytes;
+            ++alloc_count;
+        } else {
+            ++reuse_count;
+        }
+        peak_reserved = std::max(peak_reserved, reserved);
+    }
+    template <typename T>
+    T* lease(size_t count) {
+        const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        if (used + bytes > reserved) throw Fail(GSRC_ERR_RESOURCE, "arena exhausted");
+        T* p = reinterpret_cast<T*>(base + used);
+        used += bytes;
+        ++leases;
+        peak_active = std::max(peak_active, used);
+        return p;
+    }
+    void release_all() {
+        release_count += leases;
+        leases = 0;
+        used = 0;
+    }
+    ~Arena() { if (base) cudaFree(base); }
+};
+
+size_t bytes_rounded(size_t b) { return (b + 255) & ~size_t(255); }
+
+struct DevBuf {  // scratch for op-level parity entry points
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        CK(cudaMalloc(&p, bytes ? bytes : 16));
+        CK(cudaMemset(p, 0, bytes ? bytes : 16));
+        CK(cudaDeviceSynchronize());
+    }
+    ~DevBuf() { if (p) cudaFree(p); }
+    template <typename T> T* as() { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct gsrc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own = nullptr;
+    std::string err;
+    int64_t launches = 0;
+
+    // persistent: graph
+    int64_t n = 0, e = 0;
+    int norm = 0;
+    int *rp = nullptr, *ci = nullptr, *trp = nullptr, *tci = nullptr;
+    float *row_f = nullptr, *col_f = nullptr;
+    size_t graph_bytes = 0;
+
+    // persistent: model state
+    bool model = false;
+    gsrc_model_cfg cfg{};
+    int C = 0, nb = 0, w = 0, ld = 0, k = 0;
+    int64_t P = 0;
+    float *params = nullptr, *grads = nullptr, *opt_m = nullptr, *opt_v = nullptr, *bc = nullptr;
+    long long* d_step = nullptr;
+    size_t model_bytes = 0;
+
+    // persistent: node data
+    float *X0 = nullptr, *y = nullptr;
+    uint8_t* mask = nullptr;
+    float cnt = 0.f, captured_cnt = -1.f;
+    bool data = false;
+    size_t data_bytes = 0;
+
+    // activation arena
+    Arena arena;
+    float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr;
+    uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
+    std::vector<uint8_t*> c1, c2;
+    std::vector<char> filled;
+    double* part = nullptr;
+    int nparts = 0, nparts_small = 0;
+    float *yhat = nullptr, *gy = nullptr;
+    double *loss_part = nullptr, *loss_dev = nullptr;
+    int loss_nparts = 0;
+    double* loss_host = nullptr;  // pinned
+
+    // graph replay
+    bool use_graph = false;
+    cudaGraphExec_t g_fb = nullptr, g_step = nullptr;
+    int64_t g_fb_launches = 0, g_step_launches = 0;
+    gsrc_optim_cfg g_step_opt{};
+
+    cudaEvent_t ev[4] = {};
+    gsrc_timing timing{};
+
+    ~gsrc_ctx() {
+        if (g_fb) cudaGraphExecDestroy(g_fb);
+        if (g_step) cudaGraphExecDestroy(g_step);
+        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)params, (void*)grads,
+                        (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
+            if (p) cudaFree(p);
+        if (loss_host) cudaFreeHost(loss_host);
+        for (auto& e_ : ev) if (e_) cudaEventDestroy(e_);
+        if (own) cudaStreamDestroy(own);
+    }
+
+    // ---- helpers -----------------------------------------------------------
+    float* plane(float* base, int p) const { return base + static_cast<size_t>(p) * n * ld; }
+    int64_t off_block(int l, int i) const {
+        return static_cast<int64_t>(cfg.d_in) * cfg.hidden + cfg.hidden + (static_cast<int64_t>(l) * nb + i) * (static_cast<int64_t>(w) * w + w);
+    }
+    const float* Wb(int l, int i) const { return params + off_block(l, i); }
+    const float* Bb(int l, int i) const { return cfg.use_bias ? params + off_block(l, i) + static_cast<int64_t>(w) * w : nullptr; }
+    Dir fwd() const { return Dir{rp, ci, row_f, col_f}; }
+    Dir bwd() const { return Dir{trp, tci, col_f, row_f}; }
+
+    TileArgs tile_base() const {
+        TileArgs a;
+        a.n = static_cast<int>(n);
+        a.w = w;
+        a.ld = ld;
+        return a;
+    }
+    void run_tile(const TileArgs& a) {
+        CK(launch_tile(a, tile_grid(a.n, a.w), stream));
+        ++launches;
+    }
+    void run_gs(std::initializer_list<const float*> planes, uint8_t* rec) {
+        GsArgs g;
+        g.n = static_cast<int>(n);
+        g.w = w;
+        g.ld = ld;
+        g.k = k;
+        int i = 0;
+        for (const float* p : planes) g.planes[i++] = p;
+        g.nplanes = i;
+        g.rec = rec;
+        CK(launch_gs(g, stream));
+        ++launches;
+    }
+    void run_gs_groupsum(const float* base, uint8_t* rec) {  // GS(Σ_{j≥2} x_j), planes 1..C-1
+        GsArgs g;
+        g.n = static_cast<int>(n);
+        g.w = w;
+        g.ld = ld;
+        g.k = k;
+        for (int p = 1; p < C; ++p) g.planes[p - 1] = plane(const_cast<float*>(base), p);
+        g.nplanes = C - 1;
+        g.rec = rec;
+        CK(launch_gs(g, stream));
+        ++launches;
+    }
+    void run_sum_planes(const float* base, float* out) {
+        GsArgs g;
+        g.n = static_cast<int>(n);
+        g.w = w;
+        g.ld = ld;
+        for (int p = 1; p < C; ++p) g.planes[p - 1] = plane(const_cast<float*>(base), p);
+        g.nplanes = C - 1;
+        CK(launch_sum_planes(g, out, stream));
+        ++launches;
+    }
+    void reduce_block_grads(int l, int i) {
+        const int plen = w * w + w;
+        float* dst = grads + off_block(l, i);
+        if (cfg.use_weight) CK(launch_reduce_parts(part, nparts, plen, plen, dst, 1, stream));
+        else CK(launch_reduce_parts(part + static_cast<size_t>(w) * w, nparts, plen, w, dst + static_cast<size_t>(w) * w, 1, stream));
+        ++launches;
+    }
+
+    // ---- GSR-C / REV layers ---------------------------------------------------
+    void rev_layer_forward(int l) {
+        const bool sparse = cfg.mode == GSRC_MODE_GSRC;
+        uint8_t* cur = recA;
+        uint8_t* nxt = recB;
+        if (sparse) run_gs_groupsum(X, cur);
+        else run_sum_planes(X, U);
+        for (int i = 0; i < C; ++i) {
+            TileArgs a = tile_base();
+            a.dir = fwd();
+            if (sparse) {
+                a.agg = AGG_SPARSE;
+                a.rec_in = cur;
+                a.k_in = k;
+                if (i + 1 < C) { a.gs_out = nxt; a.k_gs = k; }
+            } else {
+                a.agg = AGG_DENSE_RELU;
+                a.x_in = (i == 0) ? U : plane(X, i - 1);
+            }
+            a.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE;
+            a.Wm = Wb(l, i);
+            a.bias = Bb(l, i);
+            a.epi = EPI_ADD;
+            a.R = plane(X, i);
+            a.out = plane(X, i);
+            run_tile(a);
+            std::swap(cur, nxt);
+        }
+    }
+    // inverse of one block: x_i = y'_i − f_i(u)
+    void rev_block_inverse(int l, int i, bool with_grads) {
+        const bool sparse = cfg.mode == GSRC_MODE_GSRC;
+        const float* u = nullptr;
+        if (sparse) {
+            if (i > 0) run_gs({plane(X, i - 1)}, recA);
+            else run_gs_groupsum(X, recA);
+        } else {
+            if (i > 0) u = plane(X, i - 1);
+            else { run_sum_planes(X, U); u = U; }
+        }
+        TileArgs a = tile_base();
+        a.dir = fwd();
+        if (sparse) { a.agg = AGG_SPARSE; a.rec_in = recA; a.k_in = k; }
+        else { a.agg = AGG_DENSE_RELU; a.x_in = u; }
+        a.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE;
+        a.Wm = Wb(l, i);
+        a.bias = Bb(l, i);
+        a.epi = EPI_SUB;
+        a.R = plane(X, i);
+        a.out = plane(X, i);
+        if (with_grads) {
+            a.G = plane(G, i);
+            a.want_db = cfg.use_bias;
+            a.part = part;
+        }
+        run_tile(a);
+        if (!with_grads) return;
+        reduce_block_grads(l, i);
+        // input gradient: du = act'(u) ⊙ ((Âᵀ G_i)·W_iᵀ) into G_{i-1} or every G_j, j ≥ 2
+        TileArgs b = tile_base();
+        b.agg = AGG_DENSE;
+        b.dir = bwd();
+        b.x_in = plane(G, i);
+        b.gemm = cfg.use_weight ? GEMM_WT : GEMM_NONE;
+        b.Wm = Wb(l, i);
+        if (sparse) { b.epi = EPI_MASKED_ADD; b.rrec = recA; b.k_r = k; }
+        else { b.epi = EPI_MASKED_ADD_RELU; b.mask_plane = u; }
+        if (i > 0) { b.dst[0] = plane(G, i - 1); b.ndst = 1; }
+        else { for (int p = 1; p < C; ++p) b.dst[p - 1] = plane(G, p); b.ndst = C - 1; }
+        run_tile(b);
+    }
+    void rev_layer_inverse(int l) { for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, false); }
+    void rev_layer_backward(int l) { for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, true); }
+
+    // ---- Algorithms 1-2 --------------------------------------------------------
+    void alg12_layer_forward(int l) {
+        if (filled[l]) seq_err("gsr_forward_layer: cache already occupied for layer " + std::to_string(l));
+        float* X1 = plane(X, 0);
+        float* X2 = plane(X, 1);
+        run_gs({X1}, c1[l]);                                 // line 5
+        TileArgs a = tile_base();                            // lines 6-8: x2' = x2 + A(GS(x1)); GS(x2')
+        a.agg = AGG_SPARSE; a.dir = fwd(); a.rec_in = c1[l]; a.k_in = k;
+        a.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE; a.Wm = Wb(l, 0); a.bias = Bb(l, 0);
+        a.epi = EPI_ADD; a.R = X2; a.out = X2; a.gs_out = c2[l]; a.k_gs = k;
+        run_tile(a);
+        TileArgs b = tile_base();                            // lines 9-10: x1' = scatter(s1) + B(GS(x2'))
+        b.agg = AGG_SPARSE; b.dir = fwd(); b.rec_in = c2[l]; b.k_in = k;
+        b.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE; b.Wm = Wb(l, 1); b.bias = Bb(l, 1);
+        b.epi = EPI_SCATTER_ADD; b.rrec = c1[l]; b.k_r = k; b.out = X1;
+        run_tile(b);
+        filled[l] = 1;
+    }
+    // gsr_backward_block for block i with upstream m:
+    //   out = Âᵀ·scatter(gather(m·Wᵀ, I_src)); dW += (Â·S_fwd)ᵀ·m; db += colsum(m)
+    void alg12_block_backward(int l, int i, const float* m, const uint8_t* isrc, const uint8_t* fwd_rec, float* out) {
+        TileArgs a = tile_base();
+        a.agg = AGG_NONE; a.x_in = m;
+        a.gemm = cfg.use_weight ? GEMM_WT : GEMM_NONE; a.Wm = Wb(l, i);
+        a.epi = EPI_GATHER_REC; a.rrec = isrc; a.k_r = k; a.out_rec = vg;
+        run_tile(a);
+        TileArgs b = tile_base();
+        b.agg = AGG_SPARSE; b.dir = bwd(); b.rec_in = vg; b.k_in = k; b.gemm = GEMM_NONE;
+        b.epi = EPI_NONE; b.out = out;
+        run_tile(b);
+        TileArgs c = tile_base();
+        c.agg = AGG_SPARSE; c.dir = fwd(); c.rec_in = fwd_rec; c.k_in = k; c.gemm = GEMM_NONE;
+        c.epi = EPI_DISCARD; c.G = m; c.want_db = cfg.use_bias; c.part = part;
+        run_tile(c);
+        reduce_block_grads(l, i);
+    }
+    void alg12_layer_backward(int l) {
+        if (!filled[l]) seq_err("gsr_backward_layer: missing forward cache for layer " + std::to_string(l));
+        float* g1 = plane(G, 0);
+        float* g2 = plane(G, 1);
+        run_gs({g2}, t2);                                    // line 4
+        TileArgs a = tile_base();                            // line 5-6: M1 = g1 − B(GS(g2)); GS(M1)
+        a.agg = AGG_SPARSE; a.dir = fwd(); a.rec_in = t2; a.k_in = k;
+        a.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE; a.Wm = Wb(l, 1); a.bias = Bb(l, 1);
+        a.epi = EPI_SUB; a.R = g1; a.out = M1; a.gs_out = t1; a.k_gs = k;
+        run_tile(a);
+        TileArgs b = tile_base();                            // lines 6-7: M2 = scatter(GS(g2)) − A(GS(M1))
+        b.agg = AGG_SPARSE; b.dir = fwd(); b.rec_in = t1; b.k_in = k;
+        b.gemm = cfg.use_weight ? GEMM_W : GEMM_NONE; b.Wm = Wb(l, 0); b.bias = Bb(l, 0);
+        b.epi = EPI_SCATTER_SUB; b.rrec = t2; b.k_r = k; b.out = M2;
+        run_tile(b);
+        const bool local = cfg.index_source == 0;            // line 8
+        alg12_block_backward(l, 0, M1, local ? t1 : c1[l], c1[l], g1);
+        alg12_block_backward(l, 1, M2, local ? t2 : c2[l], c2[l], g2);
+        filled[l] = 0;
+    }
+
+    // ---- network ---------------------------------------------------------------
+    void layer_forward(int l) { if (cfg.mode == GSRC_MODE_ALG12) alg12_layer_forward(l); else rev_layer_forward(l); }
+    void layer_backward(int l) { if (cfg.mode == GSRC_MODE_ALG12) alg12_layer_backward(l); else rev_layer_backward(l); }
+
+    void enqueue_forward() {
+        CK(launch_encoder(X0, static_cast<int>(n), cfg.d_in, params, params + static_cast<size_t>(cfg.d_in) * cfg.hidden, cfg.hidden,
+                          C, w, ld, X, stream));
+        ++launches;
+        if (cfg.mode == GSRC_MODE_ALG12) std::fill(filled.begin(), filled.end(), 0);
+        for (int l = 0; l < cfg.layers; ++l) layer_forward(l);
+        const float* wh = params + off_block(cfg.layers, 0);
+        CK(launch_head_loss(X, static_cast<int>(n), cfg.hidden, C, w, ld, wh, wh + cfg.hidden, y, mask, 0.f, cnt, yhat, gy, loss_part,
+                            loss_nparts, stream));
+        ++launches;
+        CK(launch_sum_double(loss_part, loss_nparts, 1.0 / static_cast<double>(cnt), loss_dev, stream));
+        ++launches;
+    }
+    void enqueue_backward() {
+        const float* wh = params + off_block(cfg.layers, 0);
+        CK(launch_head_bwd(X, gy, static_cast<int>(n), cfg.hidden, C, w, ld, wh, G, part, nparts_small, stream));
+        ++launches;
+        CK(launch_reduce_parts(part, nparts_small, cfg.hidden + 1, cfg.hidden + 1, grads + off_block(cfg.layers, 0), 0, stream));
+        ++launches;
+        for (int l = cfg.layers - 1; l >= 0; --l) layer_backward(l);
+        const int elen = cfg.d_in * cfg.hidden + cfg.hidden;
+        CK(launch_encoder_bwd(X0, G, static_cast<int>(n), cfg.d_in, cfg.hidden, C, w, ld, part, nparts_small, stream));
+        ++launches;
+        CK(launch_reduce_parts(part, nparts_small, elen, elen, grads, 0, stream));
+        ++launches;
+    }
+    void enqueue_zero_grads() { CK(cudaMemsetAsync(grads, 0, sizeof(float) * P, stream)); }
+    void enqueue_optimizer(const gsrc_optim_cfg& o) {
+        if (o.optimizer == 0) {
+            CK(launch_adam_prep(d_step, static_cast<double>(o.beta1), static_cast<double>(o.beta2), bc, stream));
+            CK(launch_adam(params, grads, opt_m, opt_v, P, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, bc, stream));
+            launches += 2;
+        } else {
+            CK(launch_sgd(params, grads, opt_m, P, o.lr, o.momentum, stream));
+            ++launches;
+        }
+    }
+
+    void require_model() const {
+        if (!model) seq_err("model not initialised (gsrc_model_init)");
+    }
+    void require_data() const {
+        require_model();
+        if (!data) seq_err("node data not uploaded (gsrc_data_upload)");
+    }
+    void drop_graphs() {
+        if (g_fb) { cudaGraphExecDestroy(g_fb); g_fb = nullptr; }
+        if (g_step) { cudaGraphExecDestroy(g_step); g_step = nullptr; }
+    }
+
+    // Activation arena plan (bytes independent of L except the ALG12 caches,
+    // which Alg. 1 retains by design: O(L·n·k)).
+    void plan_arena() {
+        const size_t pl = static_cast<size_t>(n) * ld;
+        const size_t rb = static_cast<size_t>(n) * rec_bytes(k > 0 ? k : 1);
+        nparts = tile_grid(static_cast<int>(n), w);
+        nparts_small = 148 * 8;
+        loss_nparts = static_cast<int>((n + kThreads - 1) / kThreads);
+        const size_t plen = static_cast<size_t>(w) * w + w;
+        size_t part_len = std::max(static_cast<size_t>(nparts) * plen, static_cast<size_t>(nparts_small) * (cfg.d_in * cfg.hidden + cfg.hidden));
+        part_len = std::max(part_len, static_cast<size_t>(nparts_small) * (cfg.hidden + 1));
+        const bool alg12 = cfg.mode == GSRC_MODE_ALG12;
+        size_t total = 0;
+        total += 2 * bytes_rounded(pl * C * sizeof(float));               // X, G
+        total += 2 * bytes_rounded(rb);                                    // recA, recB
+        total += bytes_rounded(part_len * sizeof(double));
+        total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
+        total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
+        if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
+        if (alg12) total += 2 * bytes_rounded(pl * sizeof(float)) + 3 * bytes_rounded(rb) + 2 * static_cast<size_t>(cfg.layers) * bytes_rounded(rb);
+        arena.plan(total);
+        X = arena.lease<float>(pl * C);
+        G = arena.lease<float>(pl * C);
+        recA = arena.lease<uint8_t>(rb);
+        recB = arena.lease<uint8_t>(rb);
+        part = arena.lease<double>(part_len);
+        yhat = arena.lease<float>(static_cast<size_t>(n));
+        gy = arena.lease<float>(static_cast<size_t>(n));
+        loss_part = arena.lease<double>(static_cast<size_t>(loss_nparts));
+        loss_dev = arena.lease<double>(1);
+        U = nullptr;
+        if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
+        c1.clear();
+        c2.clear();
+        if (alg12) {
+            M1 = arena.lease<float>(pl);
+            M2 = arena.lease<float>(pl);
+            t1 = arena.lease<uint8_t>(rb);
+            t2 = arena.lease<uint8_t>(rb);
+            vg = arena.lease<uint8_t>(rb);
+            for (int l = 0; l < cfg.layers; ++l) { c1.push_back(arena.lease<uint8_t>(rb)); c2.push_back(arena.lease<uint8_t>(rb)); }
+        }
+        filled.assign(static_cast<size_t>(cfg.layers), 0);
+        // zero planes once so padding columns are 0
+        CK(cudaMemsetAsync(arena.base, 0, arena.used, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+};
+
+namespace {
+
+template <typename F>
+int guarded(gsrc_ctx* ctx, F&& f) {
+    if (!ctx) return GSRC_ERR_CONFIG;
+    try {
+        int dev = -1;
+        cudaGetDevice(&dev);
+        if (dev != ctx->device) CK(cudaSetDevice(ctx->device));
+        f();
+        return GSRC_OK;
+    } catch (const Fail& e) {
+        ctx->err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "host allocation failure";
+        return GSRC_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return GSRC_ERR_INTERNAL;
+    }
+}
+
+template <typename T>
+T* dmalloc(size_t count, size_t* acct = nullptr) {
+    T* p = nullptr;
+    const size_t bytes = count * sizeof(T) ? count * sizeof(T) : 16;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); throw Fail(GSRC_ERR_RESOURCE, std::string("cudaMalloc failed: ") + cudaGetErrorString(e)); }
+    if (acct) *acct += bytes;
+    return p;
+}
+
+void h2d_rows(float* dplane_base, int64_t n, int C, int w, int ld, const float* host, int D, cudaStream_t s) {
+    for (int p = 0; p < C; ++p)
+        CK(cudaMemcpy2DAsync(dplane_base + static_cast<size_t>(p) * n * ld, ld * sizeof(float), host + static_cast<size_t>(p) * w,
+                             D * sizeof(float), w * sizeof(float), n, cudaMemcpyHostToDevice, s));
+}
+void d2h_rows(float* host, const float* dplane_base, int64_t n, int C, int w, int ld, int D, cudaStream_t s) {
+    for (int p = 0; p < C; ++p)
+        CK(cudaMemcpy2DAsync(host + static_cast<size_t>(p) * w, D * sizeof(float), dplane_base + static_cast<size_t>(p) * n * ld,
+                             ld * sizeof(float), w * sizeof(float), n, cudaMemcpyDeviceToHost, s));
+}
+
+// Pack host (vals, idx) n×k into device records.
+void upload_records(const float* vals, const int32_t* idx, int64_t n, int k, uint8_t* rec, cudaStream_t s) {
+    DevBuf dv(static_cast<size_t>(n) * k * sizeof(float)), di(static_cast<size_t>(n) * k * sizeof(int));
+    CK(cudaMemcpyAsync(dv.p, vals, static_cast<size_t>(n) * k * sizeof(float), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(di.p, idx, static_cast<size_t>(n) * k * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(launch_rec_pack(dv.as<float>(), di.as<int>(), static_cast<int>(n), k, rec, s));
+    CK(cudaStreamSynchronize(s));
+}
+void download_records(const uint8_t* rec, int64_t n, int k, float* vals, int32_t* idx, cudaStream_t s) {
+    DevBuf dv(static_cast<size_t>(n) * k * sizeof(float)), di(static_cast<size_t>(n) * k * sizeof(int));
+    CK(launch_rec_unpack(rec, static_cast<int>(n), k, dv.as<float>(), di.as<int>(), s));
+    CK(cudaMemcpyAsync(vals, dv.p, static_cast<size_t>(n) * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(idx, di.p, static_cast<size_t>(n) * k * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+void check_rec_idx(const int32_t* idx, int64_t n, int k, int w) {
+    for (int64_t r = 0; r < n; ++r)
+        for (int j = 0; j < k; ++j) {
+            const int32_t c = idx[r * k + j];
+            if (c < 0 || c >= w) cfg_err("SparseActivation index out of range at row " + std::to_string(r));
+            if (j > 0 && c <= idx[r * k + j - 1]) cfg_err("SparseActivation indices not strictly ascending at row " + std::to_string(r));
+        }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsrc_version(char* buf, size_t len) {
+    const char* v = "gsrnet 0.1.0 (b200 sm_100a)";
+    if (buf && len) { std::strncpy(buf, v, len - 1); buf[len - 1] = 0; }
+    return GSRC_OK;
+}
+
+int gsrc_create(int device, gsrc_ctx** out) {
+    if (!out) return GSRC_ERR_CONFIG;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return GSRC_ERR_RESOURCE; }
+    if (device < 0 || device >= ndev) return GSRC_ERR_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return GSRC_ERR_RESOURCE;
+    auto* ctx = new (std::nothrow) gsrc_ctx();
+    if (!ctx) return GSRC_ERR_RESOURCE;
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
+    ctx->stream = ctx->own;
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    if (init_kernel_attributes() != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
+    if (cudaMallocHost(&ctx->loss_host, sizeof(double)) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
+    *out = ctx;
+    return GSRC_OK;
+}
+
+void gsrc_destroy(gsrc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+}
+
+const char* gsrc_last_error(gsrc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gsrc_set_stream(gsrc_ctx* ctx, void* s) {
+    return guarded(ctx, [&] {
+        ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+        ctx->drop_graphs();
+    });
+}
+
+int gsrc_synchronize(gsrc_ctx* ctx) { return guarded(ctx, [&] { CK(cudaStreamSynchronize(ctx->stream)); }); }
+
+int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_ptr, const int32_t* col_idx, int norm) {
+    return guarded(ctx, [&] {
+        if (n <= 0) cfg_err("graph: n must be > 0");
+        if (e < 0 || e > 0x7fffffffLL) cfg_err("graph: e out of range for int32 CSR");
+        if (norm < 0 || norm > 2) cfg_err("graph: bad norm_mode");
+        if (!row_ptr || (e > 0 && !col_idx)) cfg_err("graph: null arrays");
+        if (row_ptr[0] != 0 || row_ptr[n] != e) throw Fail(GSRC_ERR_CONFIG, "graph: row_ptr endpoints (FormatError)");
+        std::vector<int> rp(static_cast<size_t>(n + 1)), trp(static_cast<size_t>(n + 1), 0), tci(static_cast<size_t>(e));
+        std::vector<float> rf(static_cast<size_t>(n)), cf(static_cast<size_t>(n));
+        for (int64_t r = 0; r < n; ++r) {
+            if (row_ptr[r + 1] < row_ptr[r]) cfg_err("graph: row_ptr decreasing at row " + std::to_string(r));
+            rp[r] = static_cast<int>(row_ptr[r]);
+            for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) {
+                const int32_t c = col_idx[q];
+                if (c < 0 || c >= n) cfg_err("graph: col_idx out of range at edge " + std::to_string(q));
+                if (q > row_ptr[r] && c <= col_idx[q - 1]) cfg_err("graph: col_idx not strictly ascending in row " + std::to_string(r));
+                trp[static_cast<size_t>(c) + 1]++;
+            }
+            const int64_t deg = row_ptr[r + 1] - row_ptr[r];
+            // same double-then-round expressions as the oracle (oracle/gsr_oracle.hpp norm_*_factor)
+            if (norm == GSRC_NORM_NONE) { rf[r] = 1.f; cf[r] = 1.f; }
+            else if (deg <= 0) { rf[r] = 0.f; cf[r] = norm == GSRC_NORM_SYM_DEGREE ? 0.f : 1.f; }
+            else if (norm == GSRC_NORM_ROW_MEAN) { rf[r] = static_cast<float>(1.0 / static_cast<double>(deg)); cf[r] = 1.f; }
+            else { rf[r] = cf[r] = static_cast<float>(1.0 / std::sqrt(static_cast<double>(deg))); }
+        }
+        rp[n] = static_cast<int>(e);
+        for (int64_t r = 0; r < n; ++r) trp[r + 1] += trp[r];
+        {
+            std::vector<int> fill(trp.begin(), trp.end() - 1);
+            for (int64_t r = 0; r < n; ++r)
+                for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) tci[static_cast<size_t>(fill[col_idx[q]]++)] = static_cast<int>(r);
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (void* p : {(void*)ctx->rp, (void*)ctx->ci, (void*)ctx->trp, (void*)ctx->tci, (void*)ctx->row_f, (void*)ctx->col_f}) if (p) cudaFree(p);
+        ctx->graph_bytes = 0;
+        ctx->rp = dmalloc<int>(n + 1, &ctx->graph_bytes);
+        ctx->ci = dmalloc<int>(e, &ctx->graph_bytes);
+        ctx->trp = dmalloc<int>(n + 1, &ctx->graph_bytes);
+        ctx->tci = dmalloc<int>(e, &ctx->graph_bytes);
+        ctx->row_f = dmalloc<float>(n, &ctx->graph_bytes);
+        ctx->col_f = dmalloc<float>(n, &ctx->graph_bytes);
+        CK(cudaMemcpy(ctx->rp, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+        if (e) CK(cudaMemcpy(ctx->ci, col_idx, sizeof(int) * e, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->trp, trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+        if (e) CK(cudaMemcpy(ctx->tci, tci.data(), sizeof(int) * e, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->row_f, rf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->col_f, cf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        const bool resize = ctx->n != n;
+        ctx->n = n;
+        ctx->e = e;
+        ctx->norm = norm;
+        ctx->drop_graphs();
+        if (resize && ctx->model) {  // node count changed: re-plan activations, drop data
+            ctx->plan_arena();
+            ctx->data = false;
+        }
+    });
+}
+
+int gsrc_model_init(gsrc_ctx* ctx, const gsrc_model_cfg* cfg) {
+    return guarded(ctx, [&] {
+        if (!cfg) cfg_err("null cfg");
+        if (ctx->n <= 0) seq_err("upload a graph before gsrc_model_init");
+        gsrc_model_cfg c = *cfg;
+        if (c.mode < 0 || c.mode > 2) cfg_err("mode");
+        if (c.layers < 0) cfg_err("layers < 0");
+        if (c.mode == GSRC_MODE_ALG12) c.groups = 2;
+        if (c.groups < 2 || c.hidden <= 0 || c.hidden % c.groups) cfg_err("hidden must be divisible by groups >= 2");
+        const int w = c.hidden / c.groups;
+        if (w > 128) cfg_err("group width > 128 not supported by the sm_100a kernels");
+        if (c.groups > kMaxDst + 1) cfg_err("groups > 9 not supported");
+        if (c.mode != GSRC_MODE_REV && (c.k < 1 || c.k > w)) cfg_err("k out of [1, width]");
+        if (c.d_in < 1 || c.d_in > 16) cfg_err("d_in must be in [1, 16]");
+        if (c.gemm != GSRC_GEMM_FP32 && c.gemm != GSRC_GEMM_TF32) cfg_err("gemm precision");
+        if (c.gemm == GSRC_GEMM_TF32) cfg_err("TF32 tensor-core path not built in this revision");
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->cfg = c;
+        ctx->C = c.groups;
+        ctx->nb = c.groups;
+        ctx->w = w;
+        ctx->ld = pad_ld(w);
+        ctx->k = c.mode == GSRC_MODE_REV ? 1 : c.k;
+        ctx->P = static_cast<int64_t>(c.d_in) * c.hidden + c.hidden + static_cast<int64_t>(c.layers) * ctx->nb * (static_cast<int64_t>(w) * w + w) +
+                 c.hidden + 1;
+        for (void* p : {(void*)ctx->params, (void*)ctx->grads, (void*)ctx->opt_m, (void*)ctx->opt_v, (void*)ctx->bc, (void*)ctx->d_step}) if (p) cudaFree(p);
+        ctx->model_bytes = 0;
+        ctx->params = dmalloc<float>(ctx->P, &ctx->model_bytes);
+        ctx->grads = dmalloc<float>(ctx->P, &ctx->model_bytes);
+        ctx->opt_m = dmalloc<float>(ctx->P, &ctx->model_bytes);
+        ctx->opt_v = dmalloc<float>(ctx->P, &ctx->model_bytes);
+        ctx->bc = dmalloc<float>(2, &ctx->model_bytes);
+        ctx->d_step = dmalloc<long long>(1, &ctx->model_bytes);
+        CK(cudaMemset(ctx->params, 0, sizeof(float) * ctx->P));
+        CK(cudaMemset(ctx->grads, 0, sizeof(float) * ctx->P));
+        CK(cudaMemset(ctx->opt_m, 0, sizeof(float) * ctx->P));
+        CK(cudaMemset(ctx->opt_v, 0, sizeof(float) * ctx->P));
+        CK(cudaMemset(ctx->d_step, 0, sizeof(long long)));
+        ctx->model = true;
+        ctx->drop_graphs();
+        ctx->plan_arena();
+    });
+}
+
+int gsrc_num_params(gsrc_ctx* ctx, int64_t* out) {
+    return guarded(ctx, [&] { ctx->require_model(); *out = ctx->P; });
+}
+
+int gsrc_params_set(gsrc_ctx* ctx, const float* host, int64_t n) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (n != ctx->P) cfg_err("params_set: expected " + std::to_string(ctx->P) + " values");
+        CK(cudaMemcpyAsync(ctx->params, host, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ctx->opt_m, 0, sizeof(float) * n, ctx->stream));
+        CK(cudaMemsetAsync(ctx->opt_v, 0, sizeof(float) * n, ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_step, 0, sizeof(long long), ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_params_get(gsrc_ctx* ctx, float* host, int64_t n) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (n != ctx->P) cfg_err("params_get: size mismatch");
+        CK(cudaMemcpyAsync(host, ctx->params, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_grads_get(gsrc_ctx* ctx, float* host, int64_t n) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (n != ctx->P) cfg_err("grads_get: size mismatch");
+        CK(cudaMemcpyAsync(host, ctx->grads, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_zero_grads(gsrc_ctx* ctx) {
+    return guarded(ctx, [&] { ctx->require_model(); ctx->enqueue_zero_grads(); CK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int gsrc_grads_device(gsrc_ctx* ctx, float** dptr, int64_t* n) {
+    return guarded(ctx, [&] { ctx->require_model(); *dptr = ctx->grads; *n = ctx->P; });
+}
+
+int gsrc_params_device(gsrc_ctx* ctx, float** dptr, int64_t* n) {
+    return guarded(ctx, [&] { ctx->require_model(); *dptr = ctx->params; *n = ctx->P; });
+}
+
+int gsrc_data_upload(gsrc_ctx* ctx, const float* x0, const float* y, const uint8_t* train_mask) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        const int64_t n = ctx->n;
+        if (!ctx->X0) {
+            ctx->data_bytes = 0;
+            ctx->X0 = dmalloc<float>(static_cast<size_t>(n) * 16, &ctx->data_bytes);
+            ctx->y = dmalloc<float>(n, &ctx->data_bytes);
+            ctx->mask = dmalloc<uint8_t>(n, &ctx->data_bytes);
+        }
+        int64_t cnt = 0;
+        for (int64_t r = 0; r < n; ++r) cnt += train_mask[r] ? 1 : 0;
+        if (cnt == 0) cfg_err("mse_loss: empty mask");
+        ctx->cnt = static_cast<float>(cnt);
+        CK(cudaMemcpyAsync(ctx->X0, x0, sizeof(float) * n * ctx->cfg.d_in, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->y, y, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->mask, train_mask, n, cudaMemcpyHostToDevice, ctx->stream));
+        // the mask count is a kernel argument of the captured step: re-capture on change
+        if (!ctx->data || ctx->captured_cnt != ctx->cnt) ctx->drop_graphs();
+        ctx->captured_cnt = ctx->cnt;
+        ctx->data = true;
+    });
+}
+
+int gsrc_forward(gsrc_ctx* ctx, float* yhat_out) {
+    return guarded(ctx, [&] {
+        ctx->require_data();
+        ctx->enqueue_forward();
+        if (yhat_out) CK(cudaMemcpyAsync(yhat_out, ctx->yhat, sizeof(float) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+static void run_maybe_graph(gsrc_ctx* ctx, cudaGraphExec_t& exec, int64_t& nl, const std::function<void()>& body) {
+    if (!ctx->use_graph) { body(); return; }
+    if (!exec) {
+        const int64_t before = ctx->launches;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        try { body(); } catch (...) { cudaStreamEndCapture(ctx->stream, &g); if (g) cudaGraphDestroy(g); throw; }
+        CK(cudaStreamEndCapture(ctx->stream, &g));
+        cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) throw_cuda(e, "cudaGraphInstantiate", __LINE__);
+        nl = ctx->launches - before;
+        ctx->launches = before;
+    }
+    CK(cudaGraphLaunch(exec, ctx->stream));
+    ctx->launches += nl;
+}
+
+int gsrc_forward_backward(gsrc_ctx* ctx, double* loss_out) {
+    return guarded(ctx, [&] {
+        ctx->require_data();
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_maybe_graph(ctx, ctx->g_fb, ctx->g_fb_launches, [&] {
+            ctx->enqueue_zero_grads();
+            ctx->enqueue_forward();
+            ctx->enqueue_backward();
+        });
+        CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        ctx->timing = gsrc_timing{0, 0, 0, 0, ms * 1e-3};
+        if (loss_out) *loss_out = *ctx->loss_host;
+    });
+}
+
+int gsrc_optimizer_step(gsrc_ctx* ctx, const gsrc_optim_cfg* opt) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (!opt) cfg_err("null optimizer cfg");
+        ctx->enqueue_optimizer(*opt);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_train_step(gsrc_ctx* ctx, const gsrc_optim_cfg* opt, double* loss_out) {
+    return guarded(ctx, [&] {
+        ctx->require_data();
+        if (!opt) cfg_err("null optimizer cfg");
+        if (ctx->g_step && std::memcmp(&ctx->g_step_opt, opt, sizeof(gsrc_optim_cfg)) != 0) {
+            cudaGraphExecDestroy(ctx->g_step);
+            ctx->g_step = nullptr;
+        }
+        ctx->g_step_opt = *opt;
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_maybe_graph(ctx, ctx->g_step, ctx->g_step_launches, [&] {
+            ctx->enqueue_zero_grads();
+            ctx->enqueue_forward();
+            ctx->enqueue_backward();
+            ctx->enqueue_optimizer(*opt);
+        });
+        CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        ctx->timing = gsrc_timing{0, 0, 0, 0, ms * 1e-3};
+        if (loss_out) *loss_out = *ctx->loss_host;
+    });
+}
+
+int gsrc_activation_get(gsrc_ctx* ctx, float* host) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        d2h_rows(host, ctx->X, ctx->n, ctx->C, ctx->w, ctx->ld, ctx->cfg.hidden, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int gsrc_activation_set(gsrc_ctx* ctx, const float* host) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        h2d_rows(ctx->X, ctx->n, ctx->C, ctx->w, ctx->ld, host, ctx->cfg.hidden, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int gsrc_gradient_get(gsrc_ctx* ctx, float* host) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        d2h_rows(host, ctx->G, ctx->n, ctx->C, ctx->w, ctx->ld, ctx->cfg.hidden, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int gsrc_gradient_set(gsrc_ctx* ctx, const float* host) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        h2d_rows(ctx->G, ctx->n, ctx->C, ctx->w, ctx->ld, host, ctx->cfg.hidden, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_set_graph_capture(gsrc_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        ctx->use_graph = enable != 0;
+        if (!ctx->use_graph) ctx->drop_graphs();
+    });
+}
+
+int gsrc_last_timing(gsrc_ctx* ctx, gsrc_timing* out) { return guarded(ctx, [&] { *out = ctx->timing; }); }
+
+int gsrc_mem_stats(gsrc_ctx* ctx, gsrc_mem_report* out) {
+    return guarded(ctx, [&] {
+        const uint64_t persist = ctx->graph_bytes + ctx->model_bytes + ctx->data_bytes;
+        out->reserved_bytes = ctx->arena.reserved + persist;
+        out->active_bytes = ctx->arena.used + persist;
+        out->peak_reserved_bytes = ctx->arena.peak_reserved + persist;
+        out->peak_active_bytes = ctx->arena.peak_active + persist;
+        out->alloc_count = ctx->arena.alloc_count;
+        out->reuse_count = ctx->arena.reuse_count;
+        out->release_count = ctx->arena.release_count;
+        out->utilization = out->peak_reserved_bytes ? static_cast<double>(out->peak_active_bytes) / out->peak_reserved_bytes : 1.0;
+    });
+}
+
+int gsrc_high_water_reset(gsrc_ctx* ctx) {
+    return guarded(ctx, [&] {
+        ctx->arena.peak_active = ctx->arena.used;
+        ctx->arena.peak_reserved = ctx->arena.reserved;
+    });
+}
+
+int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out) { return guarded(ctx, [&] { *out = ctx->launches; }); }
+
+int gsrc_layer_forward(gsrc_ctx* ctx, int layer) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (layer < 0 || layer >= ctx->cfg.layers) cfg_err("layer out of range");
+        ctx->layer_forward(layer);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int gsrc_layer_inverse(gsrc_ctx* ctx, int layer) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (layer < 0 || layer >= ctx->cfg.layers) cfg_err("layer out of range");
+        if (ctx->cfg.mode == GSRC_MODE_ALG12) cfg_err("Alg. 1 layers are not invertible (use GSRC or REV)");
+        ctx->rev_layer_inverse(layer);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int gsrc_layer_backward(gsrc_ctx* ctx, int layer) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (layer < 0 || layer >= ctx->cfg.layers) cfg_err("layer out of range");
+        ctx->layer_backward(layer);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- op-level parity entry points ----------------------------------------------
+int gsrc_op_gs_topk(gsrc_ctx* ctx, int64_t n, int w, int k, const float* x, float* vals, int32_t* idx) {
+    return guarded(ctx, [&] {
+        if (w < 1 || w > 128) cfg_err("gs_topk: width must be in [1, 128]");
+        if (k < 1 || k > w) cfg_err("gs_topk: k=" + std::to_string(k) + " out of [1," + std::to_string(w) + "]");
+        if (n <= 0) return;
+        const int ld = pad_ld(w);
+        DevBuf dx(static_cast<size_t>(n) * ld * sizeof(float)), drec(static_cast<size_t>(n) * rec_bytes(k));
+        CK(cudaMemcpy2DAsync(dx.p, ld * sizeof(float), x, w * sizeof(float), w * sizeof(float), n, cudaMemcpyHostToDevice, ctx->stream));
+        GsArgs g;
+        g.n = static_cast<int>(n); g.w = w; g.ld = ld; g.k = k; g.planes[0] = dx.as<float>(); g.nplanes = 1; g.rec = drec.as<uint8_t>();
+        CK(launch_gs(g, ctx->stream));
+        ++ctx->launches;
+        download_records(drec.as<uint8_t>(), n, k, vals, idx, ctx->stream);
+    });
+}
+
+int gsrc_op_spmm(gsrc_ctx* ctx, int transpose, int cols, const float* x, float* y) {
+    return guarded(ctx, [&] {
+        if (ctx->n <= 0) seq_err("no graph uploaded");
+        if (cols < 1 || cols > 128) cfg_err("spmm: cols must be in [1, 128]");
+        const int64_t n = ctx->n;
+        const int ld = pad_ld(cols);
+        DevBuf dx(static_cast<size_t>(n) * ld * 4), dy(static_cast<size_t>(n) * ld * 4);
+        CK(cudaMemcpy2DAsync(dx.p, ld * 4, x, cols * 4, cols * 4, n, cudaMemcpyHostToDevice, ctx->stream));
+        TileArgs a;
+        a.n = static_cast<int>(n); a.w = cols; a.ld = ld;
+        a.agg = AGG_DENSE; a.dir = transpose ? ctx->bwd() : ctx->fwd(); a.x_in = dx.as<float>();
+        a.gemm = GEMM_NONE; a.epi = EPI_NONE; a.out = dy.as<float>();
+        ctx->run_tile(a);
+        CK(cudaMemcpy2DAsync(y, cols * 4, dy.p, ld * 4, cols * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_op_spmm_sparse(gsrc_ctx* ctx, int transpose, int w, int k, const float* vals, const int32_t* idx, float* y) {
+    return guarded(ctx, [&] {
+        if (ctx->n <= 0) seq_err("no graph uploaded");
+        if (w < 1 || w > 128 || k < 1 || k > w) cfg_err("spmm_sparse: bad width / k");
+        const int64_t n = ctx->n;
+        check_rec_idx(idx, n, k, w);
+        const int ld = pad_ld(w);
+        DevBuf drec(static_cast<size_t>(n) * rec_bytes(k)), dy(static_cast<size_t>(n) * ld * 4);
+        upload_records(vals, idx, n, k, drec.as<uint8_t>(), ctx->stream);
+        TileArgs a;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.agg = AGG_SPARSE; a.dir = transpose ? ctx->bwd() : ctx->fwd(); a.rec_in = drec.as<uint8_t>(); a.k_in = k;
+        a.gemm = GEMM_NONE; a.epi = EPI_NONE; a.out = dy.as<float>();
+        ctx->run_tile(a);
+        CK(cudaMemcpy2DAsync(y, w * 4, dy.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_op_block_forward(gsrc_ctx* ctx, int w, int k, const float* vals, const int32_t* idx, const float* W, const float* b,
+                          int use_weight, int use_bias, int epilogue, const float* R, const float* rvals, const int32_t* ridx,
+                          float* out, int gs_k, float* gs_vals, int32_t* gs_idx) {
+    return guarded(ctx, [&] {
+        if (ctx->n <= 0) seq_err("no graph uploaded");
+        if (w < 1 || w > 128 || k < 1 || k > w) cfg_err("block_forward: bad width / k");
+        if (epilogue < 0 || epilogue > EPI_SCATTER_SUB) cfg_err("block_forward: bad epilogue");
+        if (gs_k < 0 || gs_k > w) cfg_err("block_forward: bad gs_k");
+        const int64_t n = ctx->n;
+        check_rec_idx(idx, n, k, w);
+        const int ld = pad_ld(w);
+        DevBuf drec(static_cast<size_t>(n) * rec_bytes(k)), dout(static_cast<size_t>(n) * ld * 4), dR(static_cast<size_t>(n) * ld * 4);
+        DevBuf dW(static_cast<size_t>(w) * w * 4), db(static_cast<size_t>(w) * 4), drr(static_cast<size_t>(n) * rec_bytes(k));
+        DevBuf dgs(static_cast<size_t>(n) * rec_bytes(gs_k > 0 ? gs_k : 1));
+        upload_records(vals, idx, n, k, drec.as<uint8_t>(), ctx->stream);
+        if (use_weight) CK(cudaMemcpy(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
+        if (use_bias) CK(cudaMemcpy(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice));
+        TileArgs a;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.agg = AGG_SPARSE; a.dir = ctx->fwd(); a.rec_in = drec.as<uint8_t>(); a.k_in = k;
+        a.gemm = use_weight ? GEMM_W : GEMM_NONE; a.Wm = dW.as<float>(); a.bias = use_bias ? db.as<float>() : nullptr;
+        a.epi = epilogue; a.out = dout.as<float>();
+        if (epilogue == EPI_ADD || epilogue == EPI_SUB) {
+            if (!R) cfg_err("block_forward: residual required");
+            CK(cudaMemcpy2D(dR.p, ld * 4, R, w * 4, w * 4, n, cudaMemcpyHostToDevice));
+            a.R = dR.as<float>();
+        }
+        if (epilogue == EPI_SCATTER_ADD || epilogue == EPI_SCATTER_SUB) {
+            if (!rvals || !ridx) cfg_err("block_forward: scatter residual required");
+            check_rec_idx(ridx, n, k, w);
+            upload_records(rvals, ridx, n, k, drr.as<uint8_t>(), ctx->stream);
+            a.rrec = drr.as<uint8_t>(); a.k_r = k;
+        }
+        if (gs_k > 0) { a.gs_out = dgs.as<uint8_t>(); a.k_gs = gs_k; }
+        ctx->run_tile(a);
+        CK(cudaMemcpy2DAsync(out, w * 4, dout.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (gs_k > 0) download_records(dgs.as<uint8_t>(), n, gs_k, gs_vals, gs_idx, ctx->stream);
+    });
+}
+
+int gsrc_op_dense_block(gsrc_ctx* ctx, int w, const float* x, const float* W, const float* b, int use_weight, int use_bias, float* out) {
+    return guarded(ctx, [&] {
+        if (ctx->n <= 0) seq_err("no graph uploaded");
+        if (w < 1 || w > 128) cfg_err("dense_block: bad width");
+        const int64_t n = ctx->n;
+        const int ld = pad_ld(w);
+        DevBuf dx(static_cast<size_t>(n) * ld * 4), dout(static_cast<size_t>(n) * ld * 4), dW(static_cast<size_t>(w) * w * 4), db(static_cast<size_t>(w) * 4);
+        CK(cudaMemcpy2D(dx.p, ld * 4, x, w * 4, w * 4, n, cudaMemcpyHostToDevice));
+        if (use_weight) CK(cudaMemcpy(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
+        if (use_bias) CK(cudaMemcpy(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice));
+        TileArgs a;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.agg = AGG_DENSE_RELU; a.dir = ctx->fwd(); a.x_in = dx.as<float>();
+        a.gemm = use_weight ? GEMM_W : GEMM_NONE; a.Wm = dW.as<float>(); a.bias = use_bias ? db.as<float>() : nullptr;
+        a.epi = EPI_NONE; a.out = dout.as<float>();
+        ctx->run_tile(a);
+        CK(cudaMemcpy2DAsync(out, w * 4, dout.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const int32_t* isrc, const float* fvals, const int32_t* fidx,
+                           const float* W, int use_weight, int use_bias, float* out, float* dW, float* db) {
+    return guarded(ctx, [&] {
+        if (ctx->n <= 0) seq_err("no graph uploaded");
+        if (w < 1 || w > 128 || k < 1 || k > w) cfg_err("block_backward: bad width / k");
+        const int64_t n = ctx->n;
+        check_rec_idx(isrc, n, k, w);
+        check_rec_idx(fidx, n, k, w);
+        const int ld = pad_ld(w);
+        const int grid = tile_grid(static_cast<int>(n), w);
+        const size_t plen = static_cast<size_t>(w) * w + w;
+        DevBuf dm(static_cast<size_t>(n) * ld * 4), dout(static_cast<size_t>(n) * ld * 4), dWm(static_cast<size_t>(w) * w * 4);
+        DevBuf rsrc(static_cast<size_t>(n) * rec_bytes(k)), rfwd(static_cast<size_t>(n) * rec_bytes(k)), rvg(static_cast<size_t>(n) * rec_bytes(k));
+        DevBuf part(grid * plen * sizeof(double)), dgrad(plen * 4);
+        std::vector<float> zeros(static_cast<size_t>(n) * k, 0.f);
+        CK(cudaMemcpy2D(dm.p, ld * 4, m, w * 4, w * 4, n, cudaMemcpyHostToDevice));
+        if (use_weight) CK(cudaMemcpy(dWm.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
+        upload_records(zeros.data(), isrc, n, k, rsrc.as<uint8_t>(), ctx->stream);
+        upload_records(fvals, fidx, n, k, rfwd.as<uint8_t>(), ctx->stream);
+        TileArgs a;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.agg = AGG_NONE; a.x_in = dm.as<float>(); a.gemm = use_weight ? GEMM_WT : GEMM_NONE; a.Wm = dWm.as<float>();
+        a.epi = EPI_GATHER_REC; a.rrec = rsrc.as<uint8_t>(); a.k_r = k; a.out_rec = rvg.as<uint8_t>();
+        ctx->run_tile(a);
+        TileArgs b;
+        b.n = static_cast<int>(n); b.w = w; b.ld = ld;
+        b.agg = AGG_SPARSE; b.dir = ctx->bwd(); b.rec_in = rvg.as<uint8_t>(); b.k_in = k; b.gemm = GEMM_NONE;
+        b.epi = EPI_NONE; b.out = dout.as<float>();
+        ctx->run_tile(b);
+        TileArgs c;
+        c.n = static_cast<int>(n); c.w = w; c.ld = ld;
+        c.agg = AGG_SPARSE; c.dir = ctx->fwd(); c.rec_in = rfwd.as<uint8_t>(); c.k_in = k; c.gemm = GEMM_NONE;
+        c.epi = EPI_DISCARD; c.G = dm.as<float>(); c.want_db = use_bias; c.part = part.as<double>();
+        ctx->run_tile(c);
+        CK(launch_reduce_parts(part.as<double>(), grid, static_cast<int>(plen), static_cast<int>(plen), dgrad.as<float>(), 0, ctx->stream));
+        CK(cudaMemcpy2DAsync(out, w * 4, dout.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<float> g(plen);
+        CK(cudaMemcpyAsync(g.data(), dgrad.p, plen * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (dW) for (size_t i = 0; i < static_cast<size_t>(w) * w; ++i) dW[i] = use_weight ? g[i] : 0.f;
+        if (db) for (int j = 0; j < w; ++j) db[j] = use_bias ? g[static_cast<size_t>(w) * w + j] : 0.f;
+    });
+}
+
+}  // extern "C"
