@@ -110,6 +110,9 @@ int gsrc_last_timing(gsrc_ctx* ctx, gsrc_timing* out);
 int gsrc_mem_stats(gsrc_ctx* ctx, gsrc_mem_report* out);                  /* Arena::stats SPEC.md:486-490 */
 int gsrc_high_water_reset(gsrc_ctx* ctx);
 int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out);                    /* kernels enqueued since create */
+/* Live per-kernel timing for the roofline report: out[16] = 4 kernel classes ×
+   {ms per launch, algorithmic bytes per launch, launches per step, flops per launch}. */
+int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out);
 
 /* ---- layer-level entry points (device activation = gsrc_activation_*) ----- */
 int gsrc_layer_forward(gsrc_ctx* ctx, int layer);    /* gsr_forward_layer SPEC.md:386 / rev_forward_layer :316 */

@@ -68,7 +68,7 @@ EXPORTS = [
     "gsrc_zero_grads", "gsrc_grads_device", "gsrc_params_device", "gsrc_data_upload", "gsrc_forward", "gsrc_forward_backward",
     "gsrc_optimizer_step", "gsrc_train_step", "gsrc_activation_get", "gsrc_activation_set", "gsrc_gradient_get",
     "gsrc_gradient_set", "gsrc_set_graph_capture", "gsrc_last_timing", "gsrc_mem_stats", "gsrc_high_water_reset",
-    "gsrc_kernel_launches", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
+    "gsrc_kernel_launches", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
     "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
 ]
 
@@ -107,6 +107,7 @@ def lib():
         L.gsrc_last_timing.argtypes = [vp, C.POINTER(Timing)]
         L.gsrc_mem_stats.argtypes = [vp, C.POINTER(MemReport)]
         L.gsrc_kernel_launches.argtypes = [vp, C.POINTER(i64)]
+        L.gsrc_profile_kernels.argtypes = [vp, i32, vp]
         for nm in ("gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward"):
             getattr(L, nm).argtypes = [vp, i32]
         L.gsrc_op_gs_topk.argtypes = [vp, i64, i32, i32, vp, vp, vp]
@@ -288,6 +289,17 @@ class Context:
         n = C.c_int64()
         self._chk(lib().gsrc_kernel_launches(self.h, C.byref(n)))
         return n.value
+
+    KERNEL_CLASSES = ("fused_block_fwd", "block_bwd_recompute", "block_bwd_input", "gs_groupsum")
+
+    def profile_kernels(self, reps=20):
+        out = np.zeros(16, np.float64)
+        self._chk(lib().gsrc_profile_kernels(self.h, int(reps), _p(out)))
+        res = {}
+        for c, name in enumerate(self.KERNEL_CLASSES):
+            ms, byts, per_step, flops = out[4 * c:4 * c + 4]
+            res[name] = dict(ms=float(ms), bytes=float(byts), launches_per_step=float(per_step), flops=float(flops))
+        return res
 
     # ---- op-level parity entry points (SPEC op names) ----------------------------
     def gs_topk(self, x, k):

@@ -134,6 +134,7 @@ struct gsrc_ctx {
     float *X0 = nullptr, *y = nullptr;
     uint8_t* mask = nullptr;
     float cnt = 0.f, captured_cnt = -1.f;
+    int64_t data_n = 0;
     bool data = false;
     size_t data_bytes = 0;
 
@@ -631,15 +632,14 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         if (e) CK(cudaMemcpy(ctx->tci, tci.data(), sizeof(int) * e, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->row_f, rf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->col_f, cf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        CK(cudaDeviceSynchronize());  // pageable copies may still be in flight when cudaMemcpy returns
         const bool resize = ctx->n != n;
         ctx->n = n;
         ctx->e = e;
         ctx->norm = norm;
         ctx->drop_graphs();
-        if (resize && ctx->model) {  // node count changed: re-plan activations, drop data
-            ctx->plan_arena();
-            ctx->data = false;
-        }
+        if (resize) ctx->data = false;
+        if (resize && ctx->model) ctx->plan_arena();  // node count changed: re-plan activations
     });
 }
 
@@ -681,6 +681,7 @@ int gsrc_model_init(gsrc_ctx* ctx, const gsrc_model_cfg* cfg) {
         CK(cudaMemset(ctx->opt_m, 0, sizeof(float) * ctx->P));
         CK(cudaMemset(ctx->opt_v, 0, sizeof(float) * ctx->P));
         CK(cudaMemset(ctx->d_step, 0, sizeof(long long)));
+        CK(cudaDeviceSynchronize());
         ctx->model = true;
         ctx->drop_graphs();
         ctx->plan_arena();
@@ -737,7 +738,9 @@ int gsrc_data_upload(gsrc_ctx* ctx, const float* x0, const float* y, const uint8
     return guarded(ctx, [&] {
         ctx->require_model();
         const int64_t n = ctx->n;
-        if (!ctx->X0) {
+        if (!ctx->X0 || ctx->data_n != n) {
+            for (void* p : {(void*)ctx->X0, (void*)ctx->y, (void*)ctx->mask}) if (p) cudaFree(p);
+            ctx->data_n = n;
             ctx->data_bytes = 0;
             ctx->X0 = dmalloc<float>(static_cast<size_t>(n) * 16, &ctx->data_bytes);
             ctx->y = dmalloc<float>(n, &ctx->data_bytes);
@@ -994,8 +997,8 @@ int gsrc_op_block_forward(gsrc_ctx* ctx, int w, int k, const float* vals, const 
         DevBuf dW(static_cast<size_t>(w) * w * 4), db(static_cast<size_t>(w) * 4), drr(static_cast<size_t>(n) * rec_bytes(k));
         DevBuf dgs(static_cast<size_t>(n) * rec_bytes(gs_k > 0 ? gs_k : 1));
         upload_records(vals, idx, n, k, drec.as<uint8_t>(), ctx->stream);
-        if (use_weight) CK(cudaMemcpy(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
-        if (use_bias) CK(cudaMemcpy(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice));
+        if (use_weight) CK(cudaMemcpyAsync(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice, ctx->stream));
+        if (use_bias) CK(cudaMemcpyAsync(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice, ctx->stream));
         TileArgs a;
         a.n = static_cast<int>(n); a.w = w; a.ld = ld;
         a.agg = AGG_SPARSE; a.dir = ctx->fwd(); a.rec_in = drec.as<uint8_t>(); a.k_in = k;
@@ -1003,7 +1006,7 @@ int gsrc_op_block_forward(gsrc_ctx* ctx, int w, int k, const float* vals, const 
         a.epi = epilogue; a.out = dout.as<float>();
         if (epilogue == EPI_ADD || epilogue == EPI_SUB) {
             if (!R) cfg_err("block_forward: residual required");
-            CK(cudaMemcpy2D(dR.p, ld * 4, R, w * 4, w * 4, n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy2DAsync(dR.p, ld * 4, R, w * 4, w * 4, n, cudaMemcpyHostToDevice, ctx->stream));
             a.R = dR.as<float>();
         }
         if (epilogue == EPI_SCATTER_ADD || epilogue == EPI_SCATTER_SUB) {
@@ -1027,9 +1030,9 @@ int gsrc_op_dense_block(gsrc_ctx* ctx, int w, const float* x, const float* W, co
         const int64_t n = ctx->n;
         const int ld = pad_ld(w);
         DevBuf dx(static_cast<size_t>(n) * ld * 4), dout(static_cast<size_t>(n) * ld * 4), dW(static_cast<size_t>(w) * w * 4), db(static_cast<size_t>(w) * 4);
-        CK(cudaMemcpy2D(dx.p, ld * 4, x, w * 4, w * 4, n, cudaMemcpyHostToDevice));
-        if (use_weight) CK(cudaMemcpy(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
-        if (use_bias) CK(cudaMemcpy(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy2DAsync(dx.p, ld * 4, x, w * 4, w * 4, n, cudaMemcpyHostToDevice, ctx->stream));
+        if (use_weight) CK(cudaMemcpyAsync(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice, ctx->stream));
+        if (use_bias) CK(cudaMemcpyAsync(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice, ctx->stream));
         TileArgs a;
         a.n = static_cast<int>(n); a.w = w; a.ld = ld;
         a.agg = AGG_DENSE_RELU; a.dir = ctx->fwd(); a.x_in = dx.as<float>();
@@ -1056,8 +1059,8 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
         DevBuf rsrc(static_cast<size_t>(n) * rec_bytes(k)), rfwd(static_cast<size_t>(n) * rec_bytes(k)), rvg(static_cast<size_t>(n) * rec_bytes(k));
         DevBuf part(grid * plen * sizeof(double)), dgrad(plen * 4);
         std::vector<float> zeros(static_cast<size_t>(n) * k, 0.f);
-        CK(cudaMemcpy2D(dm.p, ld * 4, m, w * 4, w * 4, n, cudaMemcpyHostToDevice));
-        if (use_weight) CK(cudaMemcpy(dWm.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy2DAsync(dm.p, ld * 4, m, w * 4, w * 4, n, cudaMemcpyHostToDevice, ctx->stream));
+        if (use_weight) CK(cudaMemcpyAsync(dWm.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice, ctx->stream));
         upload_records(zeros.data(), isrc, n, k, rsrc.as<uint8_t>(), ctx->stream);
         upload_records(fvals, fidx, n, k, rfwd.as<uint8_t>(), ctx->stream);
         TileArgs a;
@@ -1082,6 +1085,60 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
         CK(cudaStreamSynchronize(ctx->stream));
         if (dW) for (size_t i = 0; i < static_cast<size_t>(w) * w; ++i) dW[i] = use_weight ? g[i] : 0.f;
         if (db) for (int j = 0; j < w; ++j) db[j] = use_bias ? g[static_cast<size_t>(w) * w + j] : 0.f;
+    });
+}
+
+// Live per-kernel timing for the roofline report (bench.py): each GSR-C kernel
+// class is launched `reps` times on the context stream between CUDA events
+// with the real step's arguments (layer 0). out[c*4 + 0..3] = ms per launch,
+// algorithmic bytes per launch, launches per training step, flops per launch.
+// Classes: 0 fused forward block, 1 backward recompute block (+dW),
+// 2 backward input-gradient block, 3 GS of the group sum.
+int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
+    return guarded(ctx, [&] {
+        ctx->require_data();
+        if (ctx->cfg.mode != GSRC_MODE_GSRC) cfg_err("profile: GSRC mode only");
+        if (reps < 1) cfg_err("profile: reps < 1");
+        const double n = static_cast<double>(ctx->n), e = static_cast<double>(ctx->e), w = ctx->w, k = ctx->k, L = ctx->cfg.layers, C = ctx->C;
+        const double rb = rec_bytes(ctx->k), csr = 4.0 * (n + 1) + 4.0 * e;
+        const int l = 0;
+        ctx->run_gs({ctx->plane(ctx->X, 0)}, ctx->recA);
+        auto time_it = [&](const std::function<void()>& f) {
+            f();  // warm
+            CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+            for (int r = 0; r < reps; ++r) f();
+            CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+            CK(cudaEventSynchronize(ctx->ev[3]));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+            return static_cast<double>(ms) / reps;
+        };
+        TileArgs fa = ctx->tile_base();
+        fa.agg = AGG_SPARSE; fa.dir = ctx->fwd(); fa.rec_in = ctx->recA; fa.k_in = ctx->k;
+        fa.gemm = ctx->cfg.use_weight ? GEMM_W : GEMM_NONE; fa.Wm = ctx->Wb(l, 1); fa.bias = ctx->Bb(l, 1);
+        fa.epi = EPI_ADD; fa.R = ctx->plane(ctx->X, 1); fa.out = ctx->plane(ctx->X, 1); fa.gs_out = ctx->recB; fa.k_gs = ctx->k;
+        out[0] = time_it([&] { ctx->run_tile(fa); });
+        out[1] = csr + 2 * n * rb + 8 * n * w;
+        out[2] = L * C;
+        out[3] = 2 * n * w * w;
+        TileArgs ra = fa;
+        ra.epi = EPI_SUB; ra.gs_out = nullptr; ra.G = ctx->plane(ctx->G, 1); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
+        out[4] = time_it([&] { ctx->run_tile(ra); });
+        out[5] = csr + n * rb + 12 * n * w;
+        out[6] = L * C;
+        out[7] = 4 * n * w * w;
+        TileArgs ba = ctx->tile_base();
+        ba.agg = AGG_DENSE; ba.dir = ctx->bwd(); ba.x_in = ctx->plane(ctx->G, 1);
+        ba.gemm = ctx->cfg.use_weight ? GEMM_WT : GEMM_NONE; ba.Wm = ctx->Wb(l, 1);
+        ba.epi = EPI_MASKED_ADD; ba.rrec = ctx->recA; ba.k_r = ctx->k; ba.dst[0] = ctx->plane(ctx->G, 0); ba.ndst = 1;
+        out[8] = time_it([&] { ctx->run_tile(ba); });
+        out[9] = csr + 4 * n * w + n * rb + 8 * n * k;
+        out[10] = L * C;
+        out[11] = 2 * n * w * w;
+        out[12] = time_it([&] { ctx->run_gs_groupsum(ctx->X, ctx->recB); });
+        out[13] = (C - 1) * 4 * n * w + n * rb;
+        out[14] = L * (C + 1);
+        out[15] = 0;
     });
 }
 
