@@ -14,9 +14,15 @@
 //
 // Arithmetic contract ("FP32 strict mode", shared with the CUDA kernels so
 // that top-k masks and CSR indexing match bit-exactly):
-//   * aggregation: acc starts at +0, per edge in list order (CSR order forward,
-//     ascending source order for the transpose) acc = acc + (edge_scale * x),
-//     then y = row_scale * acc;
+//   * aggregation: a row's edge list (CSR order forward,
+//     ascending source order for the transpose) is cut into consecutive
+//     segments of kAggSeg = 32 edges; each segment sums acc_s = acc_s +
+//     (edge_scale * x) from +0 in list order; the row total folds the
+//     segment sums left to right (acc = acc_0, acc = acc + acc_s), then
+//     y = row_scale * acc. Rows of degree ≤ 32 are plain sequential sums. The
+//     segmentation is the deterministic merge order SPEC.md:128 allows; it lets
+//     the GPU split hub rows (">8000 neighbours") over many lanes
+//     while staying bit-identical to this oracle;
 //   * dense transform: out = fma-chain over the contraction index ascending,
 //     starting from +0, then + bias;
 //   * residual epilogues are one IEEE add/sub each in the order written in
@@ -226,16 +232,25 @@ Dir<T> direction(const Graph& g, const Scales<T>& s, bool transpose) {
     return {g.trow_ptr.data(), g.tcol_idx.data(), s.col_f.data(), s.row_f.data()};
 }
 
+// Canonical segment length of the aggregation order (see header).
+constexpr index_t kAggSeg = 32;
+
 // spmm: dense Â·x or Âᵀ·x; WorkCounter += e × cols.
 template <typename T>
 void spmm_row(const Dir<T>& d, index_t r, int cols, const T* x, index_t ldx, T* y) {
-    T acc[1024];
+    T acc[1024], part[1024];
     for (int m = 0; m < cols; ++m) acc[m] = T(0);
-    for (index_t q = d.ptr[r]; q < d.ptr[r + 1]; ++q) {
-        const index_t c = d.idx[q];
-        const T sc = d.edge_f[c];
-        const T* xr = x + c * ldx;
-        for (int m = 0; m < cols; ++m) acc[m] = acc[m] + sc * xr[m];
+    const index_t q0 = d.ptr[r], q1 = d.ptr[r + 1];
+    for (index_t s0 = q0; s0 < q1; s0 += kAggSeg) {
+        for (int m = 0; m < cols; ++m) part[m] = T(0);
+        for (index_t q = s0; q < std::min(q1, s0 + kAggSeg); ++q) {
+            const index_t c = d.idx[q];
+            const T sc = d.edge_f[c];
+            const T* xr = x + c * ldx;
+            for (int m = 0; m < cols; ++m) part[m] = part[m] + sc * xr[m];
+        }
+        if (s0 == q0) for (int m = 0; m < cols; ++m) acc[m] = part[m];
+        else for (int m = 0; m < cols; ++m) acc[m] = acc[m] + part[m];
     }
     const T rf = d.out_f[r];
     for (int m = 0; m < cols; ++m) y[m] = rf * acc[m];
@@ -256,15 +271,21 @@ void spmm(const Graph& g, bool transpose, int cols, const T* x, index_t ldx, T* 
 // spmm_sparse: == spmm(g, scatter(s)) computed in O(e·k).
 template <typename T>
 void spmm_sparse_row(const Dir<T>& d, index_t r, int w, int k, const T* vals, const std::int32_t* idx, T* y) {
-    T acc[1024];
+    T acc[1024], part[1024];
     for (int m = 0; m < w; ++m) acc[m] = T(0);
-    for (index_t q = d.ptr[r]; q < d.ptr[r + 1]; ++q) {
-        const index_t c = d.idx[q];
-        const T sc = d.edge_f[c];
-        for (int j = 0; j < k; ++j) {
-            const int m = idx[c * k + j];
-            acc[m] = acc[m] + sc * vals[c * k + j];
+    const index_t q0 = d.ptr[r], q1 = d.ptr[r + 1];
+    for (index_t s0 = q0; s0 < q1; s0 += kAggSeg) {
+        for (int m = 0; m < w; ++m) part[m] = T(0);
+        for (index_t q = s0; q < std::min(q1, s0 + kAggSeg); ++q) {
+            const index_t c = d.idx[q];
+            const T sc = d.edge_f[c];
+            for (int j = 0; j < k; ++j) {
+                const int m = idx[c * k + j];
+                part[m] = part[m] + sc * vals[c * k + j];
+            }
         }
+        if (s0 == q0) for (int m = 0; m < w; ++m) acc[m] = part[m];
+        else for (int m = 0; m < w; ++m) acc[m] = acc[m] + part[m];
     }
     const T rf = d.out_f[r];
     for (int m = 0; m < w; ++m) y[m] = rf * acc[m];

@@ -56,10 +56,14 @@ void transcribe_alg1(Net<T>& net, int l, T* X) {
     auto block = [&](const T* V, const std::int32_t* I, const T* W, const T* b, std::vector<T>& M) {
         M.assign(static_cast<size_t>(n) * w, T(0));
         for (index_t r = 0; r < n; ++r) {
-            std::vector<T> acc(static_cast<size_t>(w), T(0));
-            for (index_t q = g.row_ptr[r]; q < g.row_ptr[r + 1]; ++q) {
-                const index_t cc = g.col_idx[q];
-                for (int j = 0; j < k; ++j) acc[I[cc * k + j]] = acc[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
+            std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
+            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += 32) {
+                std::fill(part.begin(), part.end(), T(0));
+                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.row_ptr[r + 1]); ++q) {
+                    const index_t cc = g.col_idx[q];
+                    for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
+                }
+                for (int j = 0; j < w; ++j) acc[j] = (s0 == g.row_ptr[r]) ? part[j] : acc[j] + part[j];
             }
             for (int j = 0; j < w; ++j) acc[j] = sc.row_f[r] * acc[j];
             for (int j = 0; j < w; ++j) {
@@ -109,10 +113,14 @@ void transcribe_alg2(Net<T>& net, int l, T* Gm) {
     auto block = [&](const std::vector<T>& V, const std::vector<std::int32_t>& I, const T* W, const T* b, std::vector<T>& M) {
         M.assign(static_cast<size_t>(n) * w, T(0));
         for (index_t r = 0; r < n; ++r) {
-            std::vector<T> acc(static_cast<size_t>(w), T(0));
-            for (index_t q = g.row_ptr[r]; q < g.row_ptr[r + 1]; ++q) {
-                const index_t cc = g.col_idx[q];
-                for (int j = 0; j < k; ++j) acc[I[cc * k + j]] = acc[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
+            std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
+            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += 32) {
+                std::fill(part.begin(), part.end(), T(0));
+                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.row_ptr[r + 1]); ++q) {
+                    const index_t cc = g.col_idx[q];
+                    for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
+                }
+                for (int j = 0; j < w; ++j) acc[j] = (s0 == g.row_ptr[r]) ? part[j] : acc[j] + part[j];
             }
             for (int j = 0; j < w; ++j) acc[j] = sc.row_f[r] * acc[j];
             for (int j = 0; j < w; ++j) {
@@ -136,10 +144,14 @@ void transcribe_alg2(Net<T>& net, int l, T* Gm) {
                 vg[r * k + j] = t;
             }
         for (index_t r = 0; r < n; ++r) {
-            std::vector<T> acc(static_cast<size_t>(w), T(0));
-            for (index_t q = g.trow_ptr[r]; q < g.trow_ptr[r + 1]; ++q) {
-                const index_t cc = g.tcol_idx[q];
-                for (int j = 0; j < k; ++j) acc[I[cc * k + j]] = acc[I[cc * k + j]] + sc.row_f[cc] * vg[cc * k + j];
+            std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
+            for (index_t s0 = g.trow_ptr[r]; s0 < g.trow_ptr[r + 1]; s0 += 32) {
+                std::fill(part.begin(), part.end(), T(0));
+                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.trow_ptr[r + 1]); ++q) {
+                    const index_t cc = g.tcol_idx[q];
+                    for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.row_f[cc] * vg[cc * k + j];
+                }
+                for (int j = 0; j < w; ++j) acc[j] = (s0 == g.trow_ptr[r]) ? part[j] : acc[j] + part[j];
             }
             for (int j = 0; j < w; ++j) out[r * D + j] = sc.col_f[r] * acc[j];
         }

@@ -178,8 +178,9 @@ struct gsrc_ctx {
     }
     const float* Wb(int l, int i) const { return params + off_block(l, i); }
     const float* Bb(int l, int i) const { return cfg.use_bias ? params + off_block(l, i) + static_cast<int64_t>(w) * w : nullptr; }
-    Dir fwd() const { return Dir{rp, ci, row_f, col_f}; }
-    Dir bwd() const { return Dir{trp, tci, col_f, row_f}; }
+    // col_f ≡ 1 unless sym_degree; row_f ≡ 1 only for norm none
+    Dir fwd() const { return Dir{rp, ci, row_f, col_f, norm != GSRC_NORM_SYM_DEGREE}; }
+    Dir bwd() const { return Dir{trp, tci, col_f, row_f, norm == GSRC_NORM_NONE}; }
 
     TileArgs tile_base() const {
         TileArgs a;
@@ -188,8 +189,9 @@ struct gsrc_ctx {
         a.ld = ld;
         return a;
     }
+    int last_grid = 0;
     void run_tile(const TileArgs& a) {
-        CK(launch_tile(a, tile_grid(a.n, a.w), stream));
+        CK(launch_tile(a, stream, &last_grid));
         ++launches;
     }
     void run_gs(std::initializer_list<const float*> planes, uint8_t* rec) {
@@ -230,8 +232,8 @@ struct gsrc_ctx {
     void reduce_block_grads(int l, int i) {
         const int plen = w * w + w;
         float* dst = grads + off_block(l, i);
-        if (cfg.use_weight) CK(launch_reduce_parts(part, nparts, plen, plen, dst, 1, stream));
-        else CK(launch_reduce_parts(part + static_cast<size_t>(w) * w, nparts, plen, w, dst + static_cast<size_t>(w) * w, 1, stream));
+        if (cfg.use_weight) CK(launch_reduce_parts(part, last_grid, plen, plen, dst, 1, stream));
+        else CK(launch_reduce_parts(part + static_cast<size_t>(w) * w, last_grid, plen, w, dst + static_cast<size_t>(w) * w, 1, stream));
         ++launches;
     }
 
@@ -425,7 +427,7 @@ struct gsrc_ctx {
     void plan_arena() {
         const size_t pl = static_cast<size_t>(n) * ld;
         const size_t rb = static_cast<size_t>(n) * rec_bytes(k > 0 ? k : 1);
-        nparts = tile_grid(static_cast<int>(n), w);
+        nparts = tile_grid_max(static_cast<int>(n));
         nparts_small = 148 * 8;
         loss_nparts = static_cast<int>((n + kThreads - 1) / kThreads);
         const size_t plen = static_cast<size_t>(w) * w + w;
@@ -1053,7 +1055,7 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
         check_rec_idx(isrc, n, k, w);
         check_rec_idx(fidx, n, k, w);
         const int ld = pad_ld(w);
-        const int grid = tile_grid(static_cast<int>(n), w);
+        const int grid = tile_grid_max(static_cast<int>(n));
         const size_t plen = static_cast<size_t>(w) * w + w;
         DevBuf dm(static_cast<size_t>(n) * ld * 4), dout(static_cast<size_t>(n) * ld * 4), dWm(static_cast<size_t>(w) * w * 4);
         DevBuf rsrc(static_cast<size_t>(n) * rec_bytes(k)), rfwd(static_cast<size_t>(n) * rec_bytes(k)), rvg(static_cast<size_t>(n) * rec_bytes(k));
@@ -1078,7 +1080,7 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
         c.agg = AGG_SPARSE; c.dir = ctx->fwd(); c.rec_in = rfwd.as<uint8_t>(); c.k_in = k; c.gemm = GEMM_NONE;
         c.epi = EPI_DISCARD; c.G = dm.as<float>(); c.want_db = use_bias; c.part = part.as<double>();
         ctx->run_tile(c);
-        CK(launch_reduce_parts(part.as<double>(), grid, static_cast<int>(plen), static_cast<int>(plen), dgrad.as<float>(), 0, ctx->stream));
+        CK(launch_reduce_parts(part.as<double>(), ctx->last_grid, static_cast<int>(plen), static_cast<int>(plen), dgrad.as<float>(), 0, ctx->stream));
         CK(cudaMemcpy2DAsync(out, w * 4, dout.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
         std::vector<float> g(plen);
         CK(cudaMemcpyAsync(g.data(), dgrad.p, plen * 4, cudaMemcpyDeviceToHost, ctx->stream));

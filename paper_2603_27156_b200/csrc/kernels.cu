@@ -43,7 +43,6 @@ struct Cfg {
     static constexpr int DMB = DWE / 4;        // dW m-rows per thread (4 n-cols each)
     static constexpr int DNB = W / 4;          // dW n-blocks
     static constexpr bool kRegAcc = (W <= 64);
-    static constexpr size_t smem_floats = static_cast<size_t>(W) * W + 3ull * TR * ZLD;
 };
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -187,129 +186,233 @@ __global__ void __launch_bounds__(kThreads) k_gs(GsArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Aggregation phases (row-owned, fixed edge order).
+// Aggregation (spmm / spmm_sparse) in the canonical segmented
+// order of the oracle: each row's edge list is cut into kSeg-edge segments;
+// a segment is summed in CSR order from +0 and the row total folds its
+// segments left to right. A tile's segments are "items" (≤ kSeg edges each),
+// so a hub row of 700 (or 20 000) neighbours is spread over many lanes instead
+// of serialising one half-warp (load balance), while every column sum keeps
+// the exact oracle order (bit-identical). Items are processed in rounds of
+// ≤ kRMax: the round's neighbour ids are staged in smem with coalesced loads,
+// each item accumulates into its own smem slot (sparse: half-warp, one value
+// slot per lane, 8 neighbour records in flight; dense: warp, W/32 columns per
+// lane, 8 neighbour rows in flight), then slots fold into the tile in order.
 // ---------------------------------------------------------------------------
-// Sparse CBSR aggregation: one half-warp per row; lane j handles value slot j
-// of each neighbour record; per edge the slots hit distinct columns, and
-// edges are applied in CSR order (a __syncwarp between edges), so every
-// column's sum is accumulated in the oracle's order.
+constexpr int kSeg = 32;    // == oracle kAggSeg
+constexpr int kRMax = 64;   // items per round
+constexpr int kPF = 8;      // neighbour prefetch depth
+
 template <int W>
-__device__ __forceinline__ void agg_sparse_tile(const TileArgs& a, int row0, float* Zs) {
+struct Smem {
+    static constexpr int ZLD = Cfg<W>::ZLD;
+    static constexpr size_t ws = static_cast<size_t>(W) * W;
+    static constexpr size_t zs = static_cast<size_t>(TR) * ZLD;
+    static constexpr size_t epi = 2 * zs;                                   // Es + Gs
+    static constexpr size_t agg = static_cast<size_t>(kRMax) * W + kRMax * kSeg;  // P slots + staged ids
+    static constexpr size_t un = epi > agg ? epi : agg;
+    static constexpr size_t meta_ints = 2 * (TR + 1) + kRMax + 4;
+    static constexpr size_t floats = ws + zs + un + meta_ints;
+    static constexpr size_t bytes = floats * sizeof(float);
+};
+
+__device__ __forceinline__ int nseg_of(int deg) { return (deg + kSeg - 1) / kSeg; }
+
+template <int W, int AGG>
+__device__ __forceinline__ void aggregate_tile(const TileArgs& a, int row0, float* Zs, float* U, int* meta) {
     constexpr int ZLD = Cfg<W>::ZLD;
-    const int k = a.k_in, KH = rec_kh(k), RB = rec_bytes(k);
-    const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
-    const unsigned hmask = 0xffffu << (threadIdx.x & 16);
-    for (int rr = hw; rr < TR; rr += kThreads / 16) {
-        const int row = row0 + rr;
-        if (row >= a.n) break;
-        float* z = Zs + rr * ZLD;
-        const int e0 = __ldg(a.dir.ptr + row), e1 = __ldg(a.dir.ptr + row + 1);
-        for (int eb = e0; eb < e1; eb += 16) {
-            const int cnt = min(16, e1 - eb);
-            int myc = 0;
-            float mysc = 0.f;
-            if (l16 < cnt) {
-                myc = __ldg(a.dir.idx + eb + l16);
-                mysc = __ldg(a.dir.edge_f + myc);
-            }
-            if (k <= 16) {
-                // fast path: one value slot per lane; 4 neighbour records in flight
-                const bool act = l16 < k;
-                for (int t = 0; t < cnt; t += 4) {
-                    int ii[4];
-                    float vv[4];
+    constexpr bool SPARSE = AGG == AGG_SPARSE;
+    constexpr bool RELU = AGG == AGG_DENSE_RELU;
+    float* P = U;                                            // kRMax × W slots (segments of multi-segment rows)
+    int* cid = reinterpret_cast<int*>(U + kRMax * W);        // kRMax × kSeg staged neighbour ids
+    int* rp = meta;                                          // TR + 1 row pointers
+    int* soff = rp + TR + 1;                                 // TR + 1 segment offsets
+    int* irow = soff + TR + 1;                               // kRMax item rows
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int rows = min(TR, a.n - row0);
+
+    for (int i = tid; i <= rows; i += kThreads) rp[i] = __ldg(a.dir.ptr + row0 + i);
+    __syncthreads();
+    if (wid == 0) {
+        const int r0 = 2 * lane, r1 = 2 * lane + 1;
+        const int c0 = r0 < rows ? nseg_of(rp[r0 + 1] - rp[r0]) : 0;
+        const int c1 = r1 < rows ? nseg_of(rp[r1 + 1] - rp[r1]) : 0;
+        int incl = c0 + c1;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int c = __shfl_sync(hmask, myc, (t + u) & 15, 16);
-                        const float sc = __shfl_sync(hmask, mysc, (t + u) & 15, 16);
-                        ii[u] = 0;
-                        vv[u] = 0.f;
-                        if (act && t + u < cnt) {
-                            const uint8_t* rc = a.rec_in + static_cast<size_t>(c) * RB;
-                            ii[u] = __ldg(rc + l16);
-                            vv[u] = __fmul_rn(sc, __ldg(reinterpret_cast<const float*>(rc + KH) + l16));
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int excl = incl - c0 - c1;
+        soff[r0] = excl;
+        soff[r1] = excl + c0;
+        if (lane == 31) soff[TR] = incl;
+    }
+    __syncthreads();
+    const int total = soff[TR];
+    const bool unit = a.dir.unit_edge != 0;
+
+    for (int i0 = 0; i0 < total; i0 += kRMax) {
+        const int ni = min(kRMax, total - i0);
+        for (int s = tid; s < ni; s += kThreads) {
+            const int item = i0 + s;
+            int lo = 0, hi = rows - 1;  // last row with soff[row] <= item
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (soff[mid] <= item) lo = mid; else hi = mid - 1;
+            }
+            irow[s] = lo;
+        }
+        __syncthreads();
+        const int rf = irow[0], rl = irow[ni - 1];
+        const int Ea = rp[rf] + (i0 - soff[rf]) * kSeg;
+        const int Eb = min(rp[rl + 1], rp[rl] + (i0 + ni - soff[rl]) * kSeg);
+        for (int e = Ea + tid; e < Eb; e += kThreads) cid[e - Ea] = __ldg(a.dir.idx + e);
+        bool any_multi = false;
+        if constexpr (SPARSE) {
+            // only segments of multi-segment rows go through a slot (zeroed here);
+            // single-segment rows accumulate straight into their (zeroed) tile row
+            for (int i = tid; i < ni * (W / 4); i += kThreads) {
+                const int sl = i / (W / 4);
+                const int r = irow[sl];
+                if (rp[r + 1] - rp[r] > kSeg) *reinterpret_cast<float4*>(P + sl * W + (i % (W / 4)) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        __syncthreads();
+        if constexpr (SPARSE) {
+            const int k = a.k_in, KH = rec_kh(k), RB = rec_bytes(k);
+            const int l16 = tid & 15, hw = tid >> 4;
+            const unsigned hmask = 0xffffu << (tid & 16);
+            for (int s = hw; s < ni; s += kThreads / 16) {
+                const int r = irow[s];
+                const int e_lo = rp[r] + (i0 + s - soff[r]) * kSeg;
+                const int e_hi = min(rp[r + 1], e_lo + kSeg);
+                float* pr = (rp[r + 1] - rp[r] > kSeg) ? P + s * W : Zs + r * ZLD;
+                if (k <= 16) {
+                    const bool act = l16 < k;
+                    for (int e = e_lo; e < e_hi; e += kPF) {
+                        const int cnt = min(kPF, e_hi - e);
+                        int ii[kPF];
+                        float vv[kPF];
+#pragma unroll
+                        for (int u = 0; u < kPF; ++u) {
+                            ii[u] = 0;
+                            vv[u] = 0.f;
+                            if (act && u < cnt) {
+                                const int c = cid[e + u - Ea];
+                                const uint8_t* rc = a.rec_in + static_cast<size_t>(c) * RB;
+                                ii[u] = __ldg(rc + l16);
+                                const float v = __ldg(reinterpret_cast<const float*>(rc + KH) + l16);
+                                vv[u] = unit ? v : __fmul_rn(__ldg(a.dir.edge_f + c), v);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kPF; ++u) {
+                            if (u < cnt) {
+                                if (act) pr[ii[u]] = __fadd_rn(pr[ii[u]], vv[u]);
+                                __syncwarp(hmask);
+                            }
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (act && t + u < cnt) z[ii[u]] = __fadd_rn(z[ii[u]], vv[u]);
+                } else {
+                    for (int e = e_lo; e < e_hi; ++e) {
+                        const int c = cid[e - Ea];
+                        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
+                        const uint8_t* rc = a.rec_in + static_cast<size_t>(c) * RB;
+                        for (int j = l16; j < k; j += 16) {
+                            const int m = __ldg(rc + j);
+                            const float v = __ldg(reinterpret_cast<const float*>(rc + KH) + j);
+                            pr[m] = __fadd_rn(pr[m], unit ? v : __fmul_rn(sc, v));
+                        }
                         __syncwarp(hmask);
                     }
                 }
-            } else {
-                // k > 16: each edge is applied completely before the next one
-                for (int t = 0; t < cnt; ++t) {
-                    const int c = __shfl_sync(hmask, myc, t, 16);
-                    const float sc = __shfl_sync(hmask, mysc, t, 16);
-                    const uint8_t* rc = a.rec_in + static_cast<size_t>(c) * RB;
-                    for (int j = l16; j < k; j += 16) {
-                        const int m = __ldg(rc + j);
-                        z[m] = __fadd_rn(z[m], __fmul_rn(sc, __ldg(reinterpret_cast<const float*>(rc + KH) + j)));
-                    }
-                    __syncwarp(hmask);
-                }
+                any_multi |= (rp[r + 1] - rp[r] > kSeg);
             }
-        }
-    }
-}
-
-// Dense aggregation of a plane (optionally ReLU'd): one warp per row, lanes
-// own W/32 consecutive columns, edges in CSR order, 4 neighbour rows in
-// flight per warp.
-template <int W, bool RELU>
-__device__ __forceinline__ void agg_dense_tile(const TileArgs& a, int row0, float* Zs) {
-    constexpr int ZLD = Cfg<W>::ZLD;
-    constexpr int VEC = W / 32;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int col = lane * VEC;
-    const bool cok = col < a.ld;
-    for (int rr = wid; rr < TR; rr += kThreads / 32) {
-        const int row = row0 + rr;
-        if (row >= a.n) break;
-        float acc[VEC];
+        } else {
+            constexpr int VEC = W / 32;
+            const int col = lane * VEC;
+            const bool cok = col < a.ld;
+            for (int s = wid; s < ni; s += kThreads / 32) {
+                const int r = irow[s];
+                const int e_lo = rp[r] + (i0 + s - soff[r]) * kSeg;
+                const int e_hi = min(rp[r + 1], e_lo + kSeg);
+                float acc[VEC];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = 0.f;
-        const int e0 = __ldg(a.dir.ptr + row), e1 = __ldg(a.dir.ptr + row + 1);
-        for (int eb = e0; eb < e1; eb += 32) {
-            const int cnt = min(32, e1 - eb);
-            int myc = 0;
-            float mysc = 0.f;
-            if (lane < cnt) {
-                myc = __ldg(a.dir.idx + eb + lane);
-                mysc = __ldg(a.dir.edge_f + myc);
-            }
-            for (int t = 0; t < cnt; t += 4) {
-                float v[4][VEC];
-                float sc[4];
+                for (int q = 0; q < VEC; ++q) acc[q] = 0.f;
+                for (int e = e_lo; e < e_hi; e += kPF) {
+                    const int cnt = min(kPF, e_hi - e);
+                    float v[kPF][VEC];
+                    float sc[kPF];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = __shfl_sync(kFull, myc, (t + u) & 31);
-                    sc[u] = __shfl_sync(kFull, mysc, (t + u) & 31);
+                    for (int u = 0; u < kPF; ++u) {
 #pragma unroll
-                    for (int q = 0; q < VEC; ++q) v[u][q] = 0.f;
-                    if (t + u < cnt && cok) {
-                        const float* src = a.x_in + static_cast<size_t>(c) * a.ld + col;
-                        if constexpr (VEC == 4) { const float4 f = ld4(src); v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w; }
-                        else if constexpr (VEC == 2) { const float2 f = __ldg(reinterpret_cast<const float2*>(src)); v[u][0] = f.x; v[u][1] = f.y; }
-                        else v[u][0] = __ldg(src);
+                        for (int q = 0; q < VEC; ++q) v[u][q] = 0.f;
+                        sc[u] = 1.f;
+                        if (u < cnt) {
+                            const int c = cid[e + u - Ea];
+                            if (!unit) sc[u] = __ldg(a.dir.edge_f + c);
+                            if (cok) {
+                                const float* src = a.x_in + static_cast<size_t>(c) * a.ld + col;
+                                if constexpr (VEC == 4) { const float4 f = ld4(src); v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w; }
+                                else if constexpr (VEC == 2) { const float2 f = __ldg(reinterpret_cast<const float2*>(src)); v[u][0] = f.x; v[u][1] = f.y; }
+                                else v[u][0] = __ldg(src);
+                            }
+                        }
                     }
-                }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (t + u < cnt) {
+                    for (int u = 0; u < kPF; ++u) {
+                        if (u < cnt) {
 #pragma unroll
-                        for (int q = 0; q < VEC; ++q) {
-                            float xv = v[u][q];
-                            if (RELU) xv = xv > 0.f ? xv : 0.f;
-                            acc[q] = __fadd_rn(acc[q], __fmul_rn(sc[u], xv));
+                            for (int q = 0; q < VEC; ++q) {
+                                float xv = v[u][q];
+                                if (RELU) xv = xv > 0.f ? xv : 0.f;
+                                acc[q] = __fadd_rn(acc[q], unit ? xv : __fmul_rn(sc[u], xv));
+                            }
                         }
                     }
                 }
+                const bool multi = rp[r + 1] - rp[r] > kSeg;
+                float* dst = multi ? P + s * W : Zs + r * ZLD;
+                if (cok) {
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) dst[col + q] = acc[q];
+                }
+                any_multi |= multi;
             }
         }
-        if (cok) {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) Zs[rr * ZLD + col + q] = acc[q];
+        // fold segment slots of multi-segment rows into their tile rows, in order
+        if (__syncthreads_or(any_multi)) {
+            constexpr int TPG = W / 4;
+            constexpr int NG = kThreads / TPG;
+            const int g = tid / TPG, c4 = (tid % TPG) * 4;
+            for (int r = g; r < rows; r += NG) {
+                if (rp[r + 1] - rp[r] <= kSeg) continue;
+                const int s_lo = max(soff[r], i0), s_hi = min(soff[r + 1], i0 + ni);
+                for (int it = s_lo; it < s_hi; ++it) {
+                    const float4 pv = *reinterpret_cast<const float4*>(P + (it - i0) * W + c4);
+                    float4* z = reinterpret_cast<float4*>(Zs + r * ZLD + c4);
+                    if (it == soff[r]) *z = pv;
+                    else {
+                        float4 zv = *z;
+                        zv.x = __fadd_rn(zv.x, pv.x); zv.y = __fadd_rn(zv.y, pv.y);
+                        zv.z = __fadd_rn(zv.z, pv.z); zv.w = __fadd_rn(zv.w, pv.w);
+                        *z = zv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // row normalisation y = row_scale · acc (rows of this tile)
+    {
+        constexpr int TPG = W / 4;
+        for (int i = tid; i < rows * TPG; i += kThreads) {
+            const int r = i / TPG, c4 = (i % TPG) * 4;
+            const float f = __ldg(a.dir.out_f + row0 + r);
+            float4* z = reinterpret_cast<float4*>(Zs + r * ZLD + c4);
+            float4 zv = *z;
+            zv.x = __fmul_rn(f, zv.x); zv.y = __fmul_rn(f, zv.y); zv.z = __fmul_rn(f, zv.z); zv.w = __fmul_rn(f, zv.w);
+            *z = zv;
         }
     }
 }
@@ -322,11 +425,14 @@ template <int W, int AGG, int TPR>
 __global__ void __launch_bounds__(kThreads) k_tile(TileArgs a) {
     using C = Cfg<W>;
     constexpr int ZLD = C::ZLD;
+    using S = Smem<W>;
     extern __shared__ __align__(16) float smem[];
     float* Ws = smem;                    // W×W transform (padded with zeros)
-    float* Zs = Ws + W * W;              // aggregated tile
-    float* Es = Zs + TR * ZLD;           // epilogue tile (scatter source / outputs)
+    float* Zs = Ws + S::ws;              // aggregated tile
+    float* U = Zs + S::zs;               // union: aggregation slots | epilogue tiles
+    float* Es = U;                       // epilogue tile (scatter source / outputs)
     float* Gs = Es + TR * ZLD;           // upstream-gradient tile (dW)
+    int* meta = reinterpret_cast<int*>(U + S::un);
 
     const int tid = threadIdx.x;
     const int n_tiles = (a.n + TR - 1) / TR;
@@ -365,16 +471,11 @@ __global__ void __launch_bounds__(kThreads) k_tile(TileArgs a) {
 
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int row0 = tile * TR;
-        // ---- phase 0: clear tiles
-        for (int i = tid; i < TR * ZLD; i += kThreads) {
-            Zs[i] = 0.f;
-            if (scatter_epi) Es[i] = 0.f;
-        }
+        // ---- phase 0: clear the tile
+        for (int i = tid; i < TR * ZLD; i += kThreads) Zs[i] = 0.f;
         __syncthreads();
         // ---- phase A: aggregation
-        if constexpr (AGG == AGG_SPARSE) agg_sparse_tile<W>(a, row0, Zs);
-        else if constexpr (AGG == AGG_DENSE) agg_dense_tile<W, false>(a, row0, Zs);
-        else if constexpr (AGG == AGG_DENSE_RELU) agg_dense_tile<W, true>(a, row0, Zs);
+        if constexpr (AGG != AGG_NONE) aggregate_tile<W, AGG>(a, row0, Zs, U, meta);
         else {
             for (int i = tid; i < TR * (W / 4); i += kThreads) {
                 const int r = i / (W / 4), c = (i % (W / 4)) * 4;
@@ -385,15 +486,10 @@ __global__ void __launch_bounds__(kThreads) k_tile(TileArgs a) {
             }
         }
         __syncthreads();
-        // ---- phase A2: row normalisation (y = row_scale · acc) and scatter source
-        if constexpr (AGG != AGG_NONE) {
-            for (int i = tid; i < TR * W; i += kThreads) {
-                const int r = i / W, c = i % W;
-                const int row = row0 + r;
-                if (row < a.n) Zs[r * ZLD + c] = __fmul_rn(__ldg(a.dir.out_f + row), Zs[r * ZLD + c]);
-            }
-        }
+        // ---- phase A2: scatter source for the Alg. 1/2 epilogues
         if (scatter_epi) {
+            for (int i = tid; i < TR * ZLD; i += kThreads) Es[i] = 0.f;
+            __syncthreads();
             for (int i = tid; i < TR * 16; i += kThreads) {
                 const int r = i / 16, l = i % 16;
                 const int row = row0 + r;
@@ -405,6 +501,15 @@ __global__ void __launch_bounds__(kThreads) k_tile(TileArgs a) {
         __syncthreads();
         // ---- phase B: transform + bias + epilogue
         {
+            // residual rows issued before the transform so their latency hides under it
+            const bool res_epi = a.epi == EPI_ADD || a.epi == EPI_SUB;
+            float4 Rpre[C::RPT];
+#pragma unroll
+            for (int i = 0; i < C::RPT; ++i) {
+                const int row = row0 + tr * C::RPT + i;
+                Rpre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (res_epi && row < a.n && c0 < a.ld) Rpre[i] = *reinterpret_cast<const float4*>(a.R + static_cast<size_t>(row) * a.ld + c0);
+            }
             float acc[C::RPT][4];
             if (do_gemm) {
 #pragma unroll
@@ -448,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) k_tile(TileArgs a) {
                     case EPI_ADD:
                     case EPI_SUB:
                         if (rv) {
-                            const float4 R = *reinterpret_cast<const float4*>(a.R + off);
+                            const float4 R = Rpre[i];
                             const float Rv[4] = {R.x, R.y, R.z, R.w};
 #pragma unroll
                             for (int j = 0; j < 4; ++j) o[j] = a.epi == EPI_ADD ? __fadd_rn(Rv[j], h[j]) : __fsub_rn(Rv[j], h[j]);
@@ -777,7 +882,7 @@ __global__ void k_scale(float* __restrict__ p, long long n, float s) {
 
 template <int W, int AGG, int TPR>
 cudaError_t set_attr_t() {
-    const size_t smem = Cfg<W>::smem_floats * sizeof(float);
+    const size_t smem = Smem<W>::bytes;
     return cudaFuncSetAttribute(k_tile<W, AGG, TPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 }
 
@@ -791,26 +896,45 @@ cudaError_t set_attr_w() {
     return e;
 }
 
+int sm_count();
+
 template <int W, int AGG, int TPR>
-cudaError_t launch_tile_t(const TileArgs& a, int grid, cudaStream_t s) {
-    const size_t smem = Cfg<W>::smem_floats * sizeof(float);
-    k_tile<W, AGG, TPR><<<grid, kThreads, smem, s>>>(a);
+int occupancy_t() {
+    static int occ = 0;
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile<W, AGG, TPR>, kThreads, Smem<W>::bytes) != cudaSuccess) {
+            cudaGetLastError();
+            occ = 1;
+        }
+        if (occ < 1) occ = 1;
+    }
+    return occ;
+}
+
+// Persistent grid = SMs × resident CTAs of this instantiation (one wave).
+template <int W, int AGG, int TPR>
+cudaError_t launch_tile_t(const TileArgs& a, cudaStream_t s, int* grid_out) {
+    const int tiles = (a.n + TR - 1) / TR;
+    const int cap = sm_count() * occupancy_t<W, AGG, TPR>();
+    const int grid = tiles < cap ? tiles : cap;
+    if (grid_out) *grid_out = grid;
+    k_tile<W, AGG, TPR><<<grid, kThreads, Smem<W>::bytes, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int W>
-cudaError_t launch_tile_w(const TileArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_tile_w(const TileArgs& a, cudaStream_t s, int* g) {
     const int k = a.k_gs;
     const int tpr = (a.gs_out == nullptr) ? 0 : (k <= W / 4 ? 4 : (k <= W / 2 ? 2 : 1));
     switch (a.agg) {
         case AGG_SPARSE:
-            if (tpr == 0) return launch_tile_t<W, AGG_SPARSE, 0>(a, grid, s);
-            if (tpr == 4) return launch_tile_t<W, AGG_SPARSE, 4>(a, grid, s);
-            if (tpr == 2) return launch_tile_t<W, AGG_SPARSE, 2>(a, grid, s);
-            return launch_tile_t<W, AGG_SPARSE, 1>(a, grid, s);
-        case AGG_DENSE: return launch_tile_t<W, AGG_DENSE, 0>(a, grid, s);
-        case AGG_DENSE_RELU: return launch_tile_t<W, AGG_DENSE_RELU, 0>(a, grid, s);
-        default: return launch_tile_t<W, AGG_NONE, 0>(a, grid, s);
+            if (tpr == 0) return launch_tile_t<W, AGG_SPARSE, 0>(a, s, g);
+            if (tpr == 4) return launch_tile_t<W, AGG_SPARSE, 4>(a, s, g);
+            if (tpr == 2) return launch_tile_t<W, AGG_SPARSE, 2>(a, s, g);
+            return launch_tile_t<W, AGG_SPARSE, 1>(a, s, g);
+        case AGG_DENSE: return launch_tile_t<W, AGG_DENSE, 0>(a, s, g);
+        case AGG_DENSE_RELU: return launch_tile_t<W, AGG_DENSE_RELU, 0>(a, s, g);
+        default: return launch_tile_t<W, AGG_NONE, 0>(a, s, g);
     }
 }
 
@@ -852,22 +976,18 @@ cudaError_t init_kernel_attributes() {
     return e;
 }
 
-int tile_grid(int n, int w) {
-    const int W = w <= 32 ? 32 : (w <= 64 ? 64 : 128);
-    const size_t smem = (W == 32 ? Cfg<32>::smem_floats : W == 64 ? Cfg<64>::smem_floats : Cfg<128>::smem_floats) * sizeof(float);
-    int per_sm = static_cast<int>((227u * 1024u) / (smem + 1024));
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm > 4) per_sm = 4;
+int tile_grid_max(int n) {
     const int tiles = (n + kTileRows - 1) / kTileRows;
-    const int g = sm_count() * per_sm;
-    return tiles < g ? (tiles > 0 ? tiles : 1) : g;
+    const int cap = sm_count() * 8;
+    return tiles < cap ? (tiles > 0 ? tiles : 1) : cap;
 }
 
-cudaError_t launch_tile(const TileArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_tile(const TileArgs& a, cudaStream_t s, int* grid_out) {
+    if (grid_out) *grid_out = 0;
     if (a.n == 0) return cudaSuccess;
-    if (a.w <= 32) return launch_tile_w<32>(a, grid, s);
-    if (a.w <= 64) return launch_tile_w<64>(a, grid, s);
-    if (a.w <= 128) return launch_tile_w<128>(a, grid, s);
+    if (a.w <= 32) return launch_tile_w<32>(a, s, grid_out);
+    if (a.w <= 64) return launch_tile_w<64>(a, s, grid_out);
+    if (a.w <= 128) return launch_tile_w<128>(a, s, grid_out);
     return cudaErrorInvalidValue;
 }
 

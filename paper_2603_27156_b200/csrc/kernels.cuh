@@ -34,6 +34,7 @@ struct Dir {
     const int* idx = nullptr;
     const float* out_f = nullptr;
     const float* edge_f = nullptr;
+    int unit_edge = 0;   // edge_f ≡ 1 (multiplication by 1 is exact: skipped)
 };
 
 enum Agg : int { AGG_SPARSE = 0, AGG_DENSE = 1, AGG_DENSE_RELU = 2, AGG_NONE = 3 };
@@ -89,9 +90,9 @@ struct GsArgs {
 };
 
 // Host launchers (kernels.cu). All enqueue on `s` and return cudaError_t.
-cudaError_t launch_tile(const TileArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_tile(const TileArgs& a, cudaStream_t s, int* grid_out);  // grid = SMs × occupancy
 cudaError_t launch_gs(const GsArgs& a, cudaStream_t s);
-int tile_grid(int n, int w);   // persistent grid size for the tile kernels
+int tile_grid_max(int n);      // upper bound of any tile launch's grid (partial-buffer sizing)
 cudaError_t init_kernel_attributes();  // opt-in dynamic smem for every k_tile instantiation
 cudaError_t launch_reduce_parts(const double* part, int nparts, int stride, int len, float* out, int accumulate, cudaStream_t s);
 cudaError_t launch_sum_double(const double* in, int n, double scale, double* out, cudaStream_t s);

@@ -32,7 +32,9 @@ def param_layout(mode, layers, hidden, groups, d_in):
 
 
 def init_params(mode, layers, hidden, groups, d_in, seed=0, block_scale=None, dtype=np.float32):
-    """Uniform ±sqrt(6/(2w)) blocks, Glorot encoder / head."""
+    """Glorot encoder / head; block weights uniform ±sqrt(6/(2w))
+    divided by sqrt(L·C) by default (depth-scaled so an 80-layer, 4-group
+    reversible stack neither explodes nor vanishes at init)."""
     lay = param_layout(mode, layers, hidden, groups, d_in)
     rng = np.random.Generator(np.random.PCG64(seed))
     P = lay["P"]
@@ -41,7 +43,8 @@ def init_params(mode, layers, hidden, groups, d_in, seed=0, block_scale=None, dt
     s_enc = np.sqrt(6.0 / (d_in + hidden))
     o, n = lay["enc_w"]
     p[o:o + n] = rng.uniform(-s_enc, s_enc, n)
-    bs = block_scale if block_scale is not None else np.sqrt(6.0 / (2 * w))
+    nb = len(lay["blocks"])
+    bs = block_scale if block_scale is not None else np.sqrt(6.0 / (2 * w)) / np.sqrt(max(nb, 1))
     for _, o, w_ in lay["blocks"]:
         p[o:o + w_ * w_] = rng.uniform(-bs, bs, w_ * w_)
     o, n = lay["head_w"]
