@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--mode", default="gsrc", choices=["gsrc", "alg12", "rev"])
+    ap.add_argument("--gemm", default="tf32", choices=["tf32", "fp32"],
+                    help="block transform on tcgen05 TF32 (default) or FP32-strict CUDA cores (bit-exact parity mode)")
     ap.add_argument("--no-graph", action="store_true", help="disable CUDA-graph replay of the step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -206,7 +208,7 @@ class _CudaArray:
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2603_27156_b200 import MODE_ALG12, MODE_GSRC, MODE_REV, Context, model
+    from paper_2603_27156_b200 import GEMM_FP32, GEMM_TF32, MODE_ALG12, MODE_GSRC, MODE_REV, Context, model
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -223,7 +225,7 @@ def run_ours(args):
     ctx = Context(local)
     ctx.set_stream(stream.cuda_stream)
     ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
-    ctx.model_init(mode_id, L, D, C, k, d_in)
+    ctx.model_init(mode_id, L, D, C, k, d_in, gemm=GEMM_TF32 if args.gemm == "tf32" else GEMM_FP32)
     p0 = model.init_params(mode_id, L, D, C, d_in, seed=1)
     ctx.set_params(p0)
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
@@ -318,10 +320,10 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.gemm == "fp32" else "f32 (tf32 tensor-core transform)",
             "data": "synthetic (seeded generate_synthetic SPEC.md:186-194; random-init weights)",
             "config": {"workload": WORKLOAD[args.config], "n_nodes": g.n, "n_edges": g.e, "layers": L, "hidden": D, "groups": C, "k": k,
-                       "d_in": d_in, "mode": args.mode, "optimizer": f"adam lr={LR}", "gemm": "fp32-strict (CUDA cores)", "parallelism": f"dp{world}",
+                       "d_in": d_in, "mode": args.mode, "optimizer": f"adam lr={LR}", "gemm": "tcgen05 kind::tf32 (fp32 accumulate)" if args.gemm == "tf32" else "fp32-strict (CUDA cores)", "parallelism": f"dp{world}",
                        "subgraph_per_rank": "seed = rank", "l2": "inputs larger than L2 (activations 1 GB/plane set)",
                        "cuda_graph": not args.no_graph},
             "edges_layers_per_s": value * g.e * L,

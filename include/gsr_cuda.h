@@ -120,6 +120,7 @@ int gsrc_layer_inverse(gsrc_ctx* ctx, int layer);    /* rev_inverse_layer SPEC.m
 int gsrc_layer_backward(gsrc_ctx* ctx, int layer);   /* gsr_backward_layer SPEC.md:395 / rev_backward :334 */
 
 /* ---- op-level parity entry points (host pointers; graph = uploaded graph) -- */
+int gsrc_set_op_precision(gsrc_ctx* ctx, int gemm);   /* transform precision of the gsrc_op_* blocks (gsrc_gemm) */
 int gsrc_op_gs_topk(gsrc_ctx* ctx, int64_t n, int w, int k, const float* x, float* vals, int32_t* idx);
 int gsrc_op_spmm(gsrc_ctx* ctx, int transpose, int cols, const float* x, float* y);
 int gsrc_op_spmm_sparse(gsrc_ctx* ctx, int transpose, int w, int k, const float* vals, const int32_t* idx, float* y);

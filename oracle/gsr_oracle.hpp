@@ -16,10 +16,10 @@
 // that top-k masks and CSR indexing match bit-exactly):
 //   * aggregation: a row's edge list (CSR order forward,
 //     ascending source order for the transpose) is cut into consecutive
-//     segments of kAggSeg = 32 edges; each segment sums acc_s = acc_s +
+//     segments of kAggSeg = 8 edges; each segment sums acc_s = acc_s +
 //     (edge_scale * x) from +0 in list order; the row total folds the
 //     segment sums left to right (acc = acc_0, acc = acc + acc_s), then
-//     y = row_scale * acc. Rows of degree ≤ 32 are plain sequential sums. The
+//     y = row_scale * acc. Rows of degree ≤ 8 are plain sequential sums. The
 //     segmentation is the deterministic merge order SPEC.md:128 allows; it lets
 //     the GPU split hub rows (">8000 neighbours") over many lanes
 //     while staying bit-identical to this oracle;
@@ -233,7 +233,7 @@ Dir<T> direction(const Graph& g, const Scales<T>& s, bool transpose) {
 }
 
 // Canonical segment length of the aggregation order (see header).
-constexpr index_t kAggSeg = 32;
+constexpr index_t kAggSeg = 8;
 
 // spmm: dense Â·x or Âᵀ·x; WorkCounter += e × cols.
 template <typename T>

@@ -57,9 +57,9 @@ void transcribe_alg1(Net<T>& net, int l, T* X) {
         M.assign(static_cast<size_t>(n) * w, T(0));
         for (index_t r = 0; r < n; ++r) {
             std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
-            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += 32) {
+            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += kAggSeg) {
                 std::fill(part.begin(), part.end(), T(0));
-                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.row_ptr[r + 1]); ++q) {
+                for (index_t q = s0; q < std::min<index_t>(s0 + kAggSeg, g.row_ptr[r + 1]); ++q) {
                     const index_t cc = g.col_idx[q];
                     for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
                 }
@@ -114,9 +114,9 @@ void transcribe_alg2(Net<T>& net, int l, T* Gm) {
         M.assign(static_cast<size_t>(n) * w, T(0));
         for (index_t r = 0; r < n; ++r) {
             std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
-            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += 32) {
+            for (index_t s0 = g.row_ptr[r]; s0 < g.row_ptr[r + 1]; s0 += kAggSeg) {
                 std::fill(part.begin(), part.end(), T(0));
-                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.row_ptr[r + 1]); ++q) {
+                for (index_t q = s0; q < std::min<index_t>(s0 + kAggSeg, g.row_ptr[r + 1]); ++q) {
                     const index_t cc = g.col_idx[q];
                     for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.col_f[cc] * V[cc * k + j];
                 }
@@ -145,9 +145,9 @@ void transcribe_alg2(Net<T>& net, int l, T* Gm) {
             }
         for (index_t r = 0; r < n; ++r) {
             std::vector<T> acc(static_cast<size_t>(w), T(0)), part(static_cast<size_t>(w));
-            for (index_t s0 = g.trow_ptr[r]; s0 < g.trow_ptr[r + 1]; s0 += 32) {
+            for (index_t s0 = g.trow_ptr[r]; s0 < g.trow_ptr[r + 1]; s0 += kAggSeg) {
                 std::fill(part.begin(), part.end(), T(0));
-                for (index_t q = s0; q < std::min<index_t>(s0 + 32, g.trow_ptr[r + 1]); ++q) {
+                for (index_t q = s0; q < std::min<index_t>(s0 + kAggSeg, g.trow_ptr[r + 1]); ++q) {
                     const index_t cc = g.tcol_idx[q];
                     for (int j = 0; j < k; ++j) part[I[cc * k + j]] = part[I[cc * k + j]] + sc.row_f[cc] * vg[cc * k + j];
                 }

@@ -69,7 +69,7 @@ EXPORTS = [
     "gsrc_optimizer_step", "gsrc_train_step", "gsrc_activation_get", "gsrc_activation_set", "gsrc_gradient_get",
     "gsrc_gradient_set", "gsrc_set_graph_capture", "gsrc_last_timing", "gsrc_mem_stats", "gsrc_high_water_reset",
     "gsrc_kernel_launches", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
-    "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
+    "gsrc_set_op_precision", "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
 ]
 
 _lib = None
@@ -111,6 +111,7 @@ def lib():
         for nm in ("gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward"):
             getattr(L, nm).argtypes = [vp, i32]
         L.gsrc_op_gs_topk.argtypes = [vp, i64, i32, i32, vp, vp, vp]
+        L.gsrc_set_op_precision.argtypes = [vp, i32]
         L.gsrc_op_spmm.argtypes = [vp, i32, i32, vp, vp]
         L.gsrc_op_spmm_sparse.argtypes = [vp, i32, i32, i32, vp, vp, vp]
         L.gsrc_op_block_forward.argtypes = [vp, i32, i32, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp]
@@ -302,6 +303,9 @@ class Context:
         return res
 
     # ---- op-level parity entry points (SPEC op names) ----------------------------
+    def set_op_precision(self, gemm):
+        self._chk(lib().gsrc_set_op_precision(self.h, int(gemm)))
+
     def gs_topk(self, x, k):
         x = _f32(x)
         n, w = x.shape

@@ -15,8 +15,8 @@ LIB = os.path.join(HERE, "libgsrcuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-SOURCES = ["kernels.cu", "capi.cu"]
-HEADERS = ["kernels.cuh", os.path.join(ROOT, "include", "gsr_cuda.h")]
+SOURCES = ["kernels.cu", "tile_w32.cu", "tile_w64.cu", "tile_w128.cu", "capi.cu"]
+HEADERS = ["kernels.cuh", "common.cuh", "tile.cuh", os.path.join(ROOT, "include", "gsr_cuda.h")]
 
 
 def _mtime(p):
@@ -26,16 +26,20 @@ def _mtime(p):
 def build(verbose: bool = False) -> str:
     os.makedirs(os.path.join(CSRC, "_obj"), exist_ok=True)
     hdr_t = max(_mtime(os.path.join(CSRC, h)) if not os.path.isabs(h) else _mtime(h) for h in HEADERS)
-    objs = []
+    objs, todo = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(CSRC, "_obj", src.replace(".cu", ".o"))
         objs.append(o)
         if _mtime(o) < max(_mtime(s), hdr_t):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.check_call(cmd)
+            todo.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+    from concurrent.futures import ThreadPoolExecutor
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(run, todo))
     if _mtime(LIB) < max(_mtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
         if verbose:

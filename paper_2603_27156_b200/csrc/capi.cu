@@ -187,9 +187,11 @@ struct gsrc_ctx {
         a.n = static_cast<int>(n);
         a.w = w;
         a.ld = ld;
+        a.tc = cfg.gemm == GSRC_GEMM_TF32;
         return a;
     }
     int last_grid = 0;
+    int op_tc = 0;  // transform precision of the op-level parity entry points
     void run_tile(const TileArgs& a) {
         CK(launch_tile(a, stream, &last_grid));
         ++launches;
@@ -660,7 +662,6 @@ int gsrc_model_init(gsrc_ctx* ctx, const gsrc_model_cfg* cfg) {
         if (c.mode != GSRC_MODE_REV && (c.k < 1 || c.k > w)) cfg_err("k out of [1, width]");
         if (c.d_in < 1 || c.d_in > 16) cfg_err("d_in must be in [1, 16]");
         if (c.gemm != GSRC_GEMM_FP32 && c.gemm != GSRC_GEMM_TF32) cfg_err("gemm precision");
-        if (c.gemm == GSRC_GEMM_TF32) cfg_err("TF32 tensor-core path not built in this revision");
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->cfg = c;
         ctx->C = c.groups;
@@ -872,6 +873,13 @@ int gsrc_gradient_set(gsrc_ctx* ctx, const float* host) {
     });
 }
 
+int gsrc_set_op_precision(gsrc_ctx* ctx, int gemm) {
+    return guarded(ctx, [&] {
+        if (gemm != GSRC_GEMM_FP32 && gemm != GSRC_GEMM_TF32) cfg_err("gemm precision");
+        ctx->op_tc = gemm == GSRC_GEMM_TF32;
+    });
+}
+
 int gsrc_set_graph_capture(gsrc_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
         ctx->use_graph = enable != 0;
@@ -1002,7 +1010,7 @@ int gsrc_op_block_forward(gsrc_ctx* ctx, int w, int k, const float* vals, const 
         if (use_weight) CK(cudaMemcpyAsync(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice, ctx->stream));
         if (use_bias) CK(cudaMemcpyAsync(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice, ctx->stream));
         TileArgs a;
-        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld; a.tc = ctx->op_tc;
         a.agg = AGG_SPARSE; a.dir = ctx->fwd(); a.rec_in = drec.as<uint8_t>(); a.k_in = k;
         a.gemm = use_weight ? GEMM_W : GEMM_NONE; a.Wm = dW.as<float>(); a.bias = use_bias ? db.as<float>() : nullptr;
         a.epi = epilogue; a.out = dout.as<float>();
@@ -1036,7 +1044,7 @@ int gsrc_op_dense_block(gsrc_ctx* ctx, int w, const float* x, const float* W, co
         if (use_weight) CK(cudaMemcpyAsync(dW.p, W, static_cast<size_t>(w) * w * 4, cudaMemcpyHostToDevice, ctx->stream));
         if (use_bias) CK(cudaMemcpyAsync(db.p, b, static_cast<size_t>(w) * 4, cudaMemcpyHostToDevice, ctx->stream));
         TileArgs a;
-        a.n = static_cast<int>(n); a.w = w; a.ld = ld;
+        a.n = static_cast<int>(n); a.w = w; a.ld = ld; a.tc = ctx->op_tc;
         a.agg = AGG_DENSE_RELU; a.dir = ctx->fwd(); a.x_in = dx.as<float>();
         a.gemm = use_weight ? GEMM_W : GEMM_NONE; a.Wm = dW.as<float>(); a.bias = use_bias ? db.as<float>() : nullptr;
         a.epi = EPI_NONE; a.out = dout.as<float>();

@@ -20,7 +20,7 @@
 namespace gsrk {
 
 constexpr int kThreads = 256;
-constexpr int kTileRows = 64;
+constexpr int kTileRows = 128;
 
 __host__ __device__ inline int rec_kh(int k) { return (k + 15) & ~15; }
 __host__ __device__ inline int rec_bytes(int k) { return (rec_kh(k) + 4 * k + 15) & ~15; }
@@ -79,6 +79,7 @@ struct TileArgs {
     const float* G = nullptr;              // dW partial: dW += Zᵀ G, db += colsum(G)
     int want_db = 0;
     double* part = nullptr;                // [gridDim.x][w*w + w]
+    int tc = 0;                            // 1: transform on tcgen05 (TF32), 0: FP32-strict FFMA
 };
 
 // GS top-k of (sum of) planes: u = p0 + p1 + ... (left to right), records out.
