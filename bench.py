@@ -200,15 +200,11 @@ def run_reference(args):
     return 0
 
 
-class _CudaArray:
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2603_27156_b200 import GEMM_FP32, GEMM_TF32, MODE_ALG12, MODE_GSRC, MODE_REV, Context, model
+    from paper_2603_27156_b200.dp import DataParallelStep
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -230,18 +226,7 @@ def run_ours(args):
     ctx.set_params(p0)
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
     ctx.set_graph_capture(not args.no_graph)
-    grads_t = None
-    if world > 1:
-        gp, gn = ctx.grads_device()
-        grads_t = torch.as_tensor(_CudaArray(gp, gn), device=f"cuda:{local}")
-
-    def step():
-        if world == 1:
-            return ctx.train_step(lr=LR)
-        loss = ctx.forward_backward()
-        dist.all_reduce(grads_t, op=dist.ReduceOp.AVG)
-        ctx.optimizer_step(lr=LR)
-        return loss
+    step = DataParallelStep(ctx, lr=LR)   # world 1: fused train_step; world > 1: fwd/bwd → NCCL all-reduce(avg) → Adam
 
     losses = [step() for _ in range(args.warmup)]
     ctx.high_water_reset()
@@ -298,7 +283,7 @@ def run_ours(args):
     roof = None
     kernels = None
     hbm_peak, tf_peak, peak_src = load_peaks()
-    if rank == 0 and mode_id == MODE_GSRC:
+    if rank == 0 and mode_id == MODE_GSRC and args.profile_reps > 0:
         kernels = ctx.profile_kernels(args.profile_reps)
         share = {n: v["ms"] * v["launches_per_step"] for n, v in kernels.items()}
         top = max(share, key=share.get)

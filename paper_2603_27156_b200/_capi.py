@@ -146,6 +146,7 @@ class Context:
         if st != 0:
             raise _ERRS.get(st, GsrError)(f"gsrc_create failed with status {st} (no CUDA device?)")
         self.h = h
+        self.device = int(device)
         self.n = 0
         self.cfg = None
         self.P = 0
@@ -206,6 +207,11 @@ class Context:
         p, n = C.c_void_p(), C.c_int64()
         self._chk(lib().gsrc_grads_device(self.h, C.byref(p), C.byref(n)))
         return p.value, n.value
+
+    def grads_tensor(self):
+        """torch view (no copy) of the flat device gradient buffer, for the DP all-reduce."""
+        from .dp import device_grads_tensor
+        return device_grads_tensor(self, self.device)
 
     def params_device(self):
         p, n = C.c_void_p(), C.c_int64()

@@ -45,7 +45,25 @@ def build(verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
+    build_cli(verbose)
     return LIB
+
+
+CLI_SRC = os.path.join(ROOT, "tools", "gsrnet_cuda.cpp")
+CLI = os.path.join(ROOT, "tools", "gsrnet-cuda")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """C++ host CLI over the C-ABI (include/gsr/cuda_api.hpp), linked to libgsrcuda.so."""
+    deps = [CLI_SRC, os.path.join(ROOT, "include", "gsr", "cuda_api.hpp"), os.path.join(ROOT, "include", "gsr", "common.hpp"), LIB]
+    if _mtime(CLI) >= max(_mtime(d) for d in deps):
+        return CLI
+    cmd = ["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           CLI_SRC, "-o", CLI, "-L", HERE, "-lgsrcuda", "-Wl,-rpath,$ORIGIN/../paper_2603_27156_b200"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+    return CLI
 
 
 if __name__ == "__main__":

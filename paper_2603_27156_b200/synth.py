@@ -206,3 +206,69 @@ def config_graph(name: str, seed: int = 0) -> SynthConfig:
         return SynthConfig(n=10_000_000, base_degree=2, hub_fraction=0.0005, hub_degree_range=(500, 20_000),
                            power_law=True, seed=seed)
     raise ValueError(f"unknown config {name}")
+
+
+# ---- graph-store binary formats ------------------------------
+# GSRG: magic "GSRG", u32 LE version, u64 LE n, u64 LE e, row_ptr (n+1) × i64 LE,
+#       col_idx e × i32 LE.
+# GSRN: magic "GSRN", u64 LE n, u64 LE d_in, features n×d_in f64 LE (row-major),
+#       labels n × f64 LE, split n × u8 (0 train, 1 val, 2 test).
+GSRG_VERSION = 1
+
+
+def write_graph(path: str, g: CsrGraph) -> None:
+    with open(path, "wb") as f:
+        f.write(b"GSRG")
+        f.write(np.array([GSRG_VERSION], "<u4").tobytes())
+        f.write(np.array([g.n, g.e], "<u8").tobytes())
+        f.write(np.ascontiguousarray(g.row_ptr, "<i8").tobytes())
+        f.write(np.ascontiguousarray(g.col_idx, "<i4").tobytes())
+
+
+def read_graph(path: str) -> CsrGraph:
+    """Raises ValueError (FormatError) on bad magic, version, truncation or a malformed CSR."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    if len(buf) < 24 or buf[:4] != b"GSRG":
+        raise ValueError(f"{path}: bad GSRG magic")
+    ver = int(np.frombuffer(buf, "<u4", 1, 4)[0])
+    if ver != GSRG_VERSION:
+        raise ValueError(f"{path}: unsupported GSRG version {ver}")
+    n, e = (int(x) for x in np.frombuffer(buf, "<u8", 2, 8))
+    need = 24 + 8 * (n + 1) + 4 * e
+    if len(buf) != need:
+        raise ValueError(f"{path}: truncated GSRG ({len(buf)} of {need} bytes)")
+    rp = np.frombuffer(buf, "<i8", n + 1, 24).astype(np.int64)
+    ci = np.frombuffer(buf, "<i4", e, 24 + 8 * (n + 1)).astype(np.int32)
+    if rp[0] != 0 or rp[-1] != e or np.any(np.diff(rp) < 0):
+        raise ValueError(f"{path}: malformed row_ptr")
+    if e and (ci.min() < 0 or ci.max() >= n):
+        raise ValueError(f"{path}: col_idx out of range")
+    return CsrGraph(n=n, row_ptr=rp, col_idx=ci)
+
+
+def write_node_data(path: str, nd: NodeData) -> None:
+    n, d_in = nd.features.shape
+    with open(path, "wb") as f:
+        f.write(b"GSRN")
+        f.write(np.array([n, d_in], "<u8").tobytes())
+        f.write(np.ascontiguousarray(nd.features, "<f8").tobytes())
+        f.write(np.ascontiguousarray(nd.labels, "<f8").tobytes())
+        f.write(np.ascontiguousarray(nd.split, np.uint8).tobytes())
+
+
+def read_node_data(path: str) -> NodeData:
+    with open(path, "rb") as f:
+        buf = f.read()
+    if len(buf) < 20 or buf[:4] != b"GSRN":
+        raise ValueError(f"{path}: bad GSRN magic")
+    n, d_in = (int(x) for x in np.frombuffer(buf, "<u8", 2, 4))
+    need = 20 + 8 * n * d_in + 8 * n + n
+    if len(buf) != need:
+        raise ValueError(f"{path}: truncated GSRN ({len(buf)} of {need} bytes)")
+    feats = np.frombuffer(buf, "<f8", n * d_in, 20).reshape(n, d_in).astype(np.float32)
+    labels = np.frombuffer(buf, "<f8", n, 20 + 8 * n * d_in).astype(np.float32)
+    split = np.frombuffer(buf, np.uint8, n, 20 + 8 * n * d_in + 8 * n).copy()
+    if split.size and split.max() > 2:
+        raise ValueError(f"{path}: split code out of range")
+    return NodeData(features=feats, labels=labels, split=split)

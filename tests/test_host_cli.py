@@ -1,0 +1,91 @@
+"""C++ host API / CLI (include/gsr/cuda_api.hpp, tools/gsrnet_cuda.cpp) and the
+graph-store binary formats."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2603_27156_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "tools", "gsrnet-cuda")
+
+
+@pytest.fixture(scope="module")
+def cli():
+    from paper_2603_27156_b200 import build
+    build.build()
+    return CLI
+
+
+def _files(tmp_path, n=400, seed=0):
+    g, nd = synth.generate_synthetic(synth.SynthConfig(n=n, hub_fraction=0.01, hub_degree_range=(10, 40), seed=seed))
+    gp, np_ = str(tmp_path / "g.gsrg"), str(tmp_path / "n.gsrn")
+    synth.write_graph(gp, g)
+    synth.write_node_data(np_, nd)
+    return g, nd, gp, np_
+
+
+def test_gsrg_gsrn_round_trip(tmp_path):
+    g, nd, gp, np_ = _files(tmp_path)
+    g2 = synth.read_graph(gp)
+    nd2 = synth.read_node_data(np_)
+    assert g2.n == g.n and np.array_equal(g2.row_ptr, g.row_ptr) and np.array_equal(g2.col_idx, g.col_idx)
+    assert np.array_equal(nd2.features, nd.features) and np.array_equal(nd2.labels, nd.labels)
+    assert np.array_equal(nd2.split, nd.split)
+
+
+def test_gsrg_rejects_corruption(tmp_path):
+    _, _, gp, np_ = _files(tmp_path)
+    b = bytearray(open(gp, "rb").read())
+    open(gp, "wb").write(b[:-3])
+    with pytest.raises(ValueError, match="truncated"):
+        synth.read_graph(gp)
+    b[0:4] = b"XXXX"
+    open(gp, "wb").write(b)
+    with pytest.raises(ValueError, match="magic"):
+        synth.read_graph(gp)
+
+
+def test_cli_exit_codes_without_gpu(cli, tmp_path):
+    _, _, gp, np_ = _files(tmp_path)
+    r = subprocess.run([cli, "version"], capture_output=True, text=True)
+    assert r.returncode == 0 and "gsrnet 0.1.0" in r.stdout
+    r = subprocess.run([cli, "train", "--graph", str(tmp_path / "missing.gsrg"), "--nodes", np_], capture_output=True, text=True)
+    assert r.returncode == 3, r.stderr        # ResourceError → exit 3
+    r = subprocess.run([cli, "train", "--graph", gp, "--nodes", np_, "--model", "bogus"], capture_output=True, text=True)
+    assert r.returncode == 1, r.stderr        # ConfigError → exit 1
+    bad = tmp_path / "bad.gsrg"
+    bad.write_bytes(b"NOPE" + b"\0" * 40)
+    r = subprocess.run([cli, "train", "--graph", str(bad), "--nodes", np_], capture_output=True, text=True)
+    assert r.returncode == 1 and "magic" in r.stderr   # FormatError is a ConfigError
+
+
+@pytest.mark.gpu
+def test_cli_trains_and_matches_python_host(cli, tmp_path):
+    """Same graph, node file and initial params through the C++ host and the
+    Python host: identical first-epoch loss (both run the same C-ABI)."""
+    from paper_2603_27156_b200 import MODE_GSRC, Context, init_params
+    g, nd, gp, np_ = _files(tmp_path, n=2000)
+    L, D, C, k = 3, 64, 2, 8
+    p = init_params(MODE_GSRC, L, D, C, 8, seed=3)
+    pf = tmp_path / "p.f32"
+    p.astype(np.float32).tofile(pf)
+    rep = tmp_path / "r.jsonl"
+    r = subprocess.run([cli, "train", "--graph", gp, "--nodes", np_, "--layers", str(L), "--hidden", str(D), "--groups", str(C),
+                        "--k", str(k), "--epochs", "4", "--lr", "1e-3", "--params", str(pf), "--report", str(rep)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    recs = [json.loads(x) for x in rep.read_text().splitlines()]
+    assert [x["record"] for x in recs] == ["epoch"] * 4 + ["summary"]
+    assert recs[-1]["kernel_launches"] > 0
+    ctx = Context(0)
+    ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
+    ctx.model_init(MODE_GSRC, L, D, C, k, 8)
+    ctx.set_params(p)
+    ctx.data_upload(nd.features, nd.labels, nd.train_mask)
+    l0 = ctx.train_step(lr=1e-3)
+    assert recs[0]["train_loss"] == pytest.approx(l0, rel=1e-6)
+    assert recs[3]["train_loss"] < recs[0]["train_loss"]

@@ -1,0 +1,252 @@
+// gsrnet-cuda — C++ host CLI for the B200 GSR-GNN training step.
+//
+// Mirrors the reference's `gsrnet train` (cmd_train SPEC.md:597-605; flags
+// SPEC.md:645; exit codes 0/1/3 SPEC.md:647) for the one path this build
+// accelerates: it reads a graph-store GSRG graph and GSRN node file
+// (SPEC.md:215-218), configures the network, and runs full-batch epochs
+// (forward → masked MSE → backward with inverse recomputation → Adam) through
+// the C++ host API (include/gsr/cuda_api.hpp) over the C-ABI. One line-delimited
+// JSON record per epoch plus a summary record (RunReport SPEC.md:591-594).
+//
+//   gsrnet-cuda train --graph g.gsrg --nodes n.gsrn [--model gsrc|gsr|baseline]
+//       [--layers L] [--hidden D] [--groups C] [--k K] [--epochs E] [--lr LR]
+//       [--norm none|row_mean|sym] [--precision fp32|tf32] [--seed S]
+//       [--params init.f32] [--report out.jsonl] [--device I]
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gsr/cuda_api.hpp"
+
+namespace {
+
+using gsr::index_t;
+
+std::vector<char> slurp(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw gsr::ResourceError("cannot open " + path);
+    return std::vector<char>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+
+template <typename T>
+T get_le(const std::vector<char>& b, size_t off) {  // x86-64 / aarch64 hosts are little-endian
+    T v;
+    std::memcpy(&v, b.data() + off, sizeof(T));
+    return v;
+}
+
+struct Graph {
+    index_t n = 0;
+    std::vector<index_t> row_ptr;
+    std::vector<std::int32_t> col_idx;
+};
+
+// GSRG: "GSRG", u32 version, u64 n, u64 e, row_ptr i64[n+1], col_idx i32[e].
+Graph read_gsrg(const std::string& path) {
+    const auto b = slurp(path);
+    if (b.size() < 24 || std::memcmp(b.data(), "GSRG", 4) != 0) throw gsr::FormatError(path + ": bad GSRG magic");
+    if (get_le<std::uint32_t>(b, 4) != 1) throw gsr::FormatError(path + ": unsupported GSRG version");
+    Graph g;
+    g.n = static_cast<index_t>(get_le<std::uint64_t>(b, 8));
+    const auto e = static_cast<index_t>(get_le<std::uint64_t>(b, 16));
+    const size_t need = 24 + 8 * static_cast<size_t>(g.n + 1) + 4 * static_cast<size_t>(e);
+    if (b.size() != need) throw gsr::FormatError(path + ": truncated GSRG");
+    g.row_ptr.resize(static_cast<size_t>(g.n + 1));
+    g.col_idx.resize(static_cast<size_t>(e));
+    std::memcpy(g.row_ptr.data(), b.data() + 24, 8 * g.row_ptr.size());
+    std::memcpy(g.col_idx.data(), b.data() + 24 + 8 * g.row_ptr.size(), 4 * g.col_idx.size());
+    return g;
+}
+
+struct Nodes {
+    index_t n = 0, d_in = 0;
+    std::vector<float> x, y;
+    std::vector<std::uint8_t> train;
+    index_t split_count[3] = {0, 0, 0};
+};
+
+// GSRN: "GSRN", u64 n, u64 d_in, f64 features, f64 labels, u8 split.
+Nodes read_gsrn(const std::string& path) {
+    const auto b = slurp(path);
+    if (b.size() < 20 || std::memcmp(b.data(), "GSRN", 4) != 0) throw gsr::FormatError(path + ": bad GSRN magic");
+    Nodes d;
+    d.n = static_cast<index_t>(get_le<std::uint64_t>(b, 4));
+    d.d_in = static_cast<index_t>(get_le<std::uint64_t>(b, 12));
+    const size_t n = static_cast<size_t>(d.n), di = static_cast<size_t>(d.d_in);
+    if (b.size() != 20 + 8 * n * di + 8 * n + n) throw gsr::FormatError(path + ": truncated GSRN");
+    d.x.resize(n * di);
+    d.y.resize(n);
+    d.train.resize(n);
+    for (size_t i = 0; i < n * di; ++i) d.x[i] = static_cast<float>(get_le<double>(b, 20 + 8 * i));
+    for (size_t i = 0; i < n; ++i) d.y[i] = static_cast<float>(get_le<double>(b, 20 + 8 * n * di + 8 * i));
+    for (size_t i = 0; i < n; ++i) {
+        const auto s = static_cast<std::uint8_t>(b[20 + 8 * n * di + 8 * n + i]);
+        if (s > 2) throw gsr::FormatError(path + ": split code out of range");
+        d.train[i] = s == 0;
+        d.split_count[s]++;
+    }
+    return d;
+}
+
+// Seeded init, same scales as paper_2603_27156_b200/model.py init_params
+// (Glorot encoder/head, blocks ±sqrt(6/2w)/sqrt(L·C)); splitmix64 stream.
+std::vector<float> init_params(const gsr::cuda::NetConfig& c, index_t P, std::uint64_t seed) {
+    std::uint64_t s = seed * 0x9E3779B97F4A7C15ull + 1;
+    auto uni = [&](double lim) {
+        s += 0x9E3779B97F4A7C15ull;
+        std::uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        return static_cast<float>((static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0) * lim);
+    };
+    const int C = c.mode == gsr::cuda::Mode::Alg12 ? 2 : c.groups;
+    const int D = c.hidden, w = D / C;
+    std::vector<float> p(static_cast<size_t>(P), 0.f);
+    size_t o = 0;
+    const double se = std::sqrt(6.0 / (c.d_in + D));
+    for (int i = 0; i < c.d_in * D; ++i) p[o++] = uni(se);
+    o += static_cast<size_t>(D);
+    const double bs = std::sqrt(6.0 / (2.0 * w)) / std::sqrt(static_cast<double>(std::max(1, c.layers * C)));
+    for (int l = 0; l < c.layers; ++l)
+        for (int i = 0; i < C; ++i) {
+            for (int j = 0; j < w * w; ++j) p[o++] = uni(bs);
+            o += static_cast<size_t>(w);
+        }
+    const double sh = std::sqrt(6.0 / (D + 1));
+    for (int i = 0; i < D; ++i) p[o++] = uni(sh);
+    return p;
+}
+
+int usage() {
+    std::cerr << "usage: gsrnet-cuda train --graph G.gsrg --nodes N.gsrn [--model gsrc|gsr|baseline] [--layers L] [--hidden D]\n"
+                 "                        [--groups C] [--k K] [--epochs E] [--lr LR] [--norm none|row_mean|sym]\n"
+                 "                        [--precision fp32|tf32] [--seed S] [--params init.f32] [--report out.jsonl] [--device I]\n";
+    return 1;
+}
+
+int run(int argc, char** argv) {
+    if (argc < 2) return usage();
+    const std::string cmd = argv[1];
+    if (cmd == "version") {
+        char v[128];
+        gsrc_version(v, sizeof v);
+        std::cout << gsr::kArtifactVersion << " / " << v << "\n";
+        return 0;
+    }
+    if (cmd != "train") return usage();
+    std::map<std::string, std::string> a;
+    for (int i = 2; i < argc; ++i) {
+        std::string k = argv[i];
+        if (k.rfind("--", 0) != 0 || i + 1 >= argc) throw gsr::ConfigError("bad flag " + k);
+        a[k.substr(2)] = argv[++i];
+    }
+    auto get = [&](const char* k, const std::string& d) { return a.count(k) ? a[k] : d; };
+    if (!a.count("graph") || !a.count("nodes")) throw gsr::ConfigError("--graph and --nodes are required");
+
+    gsr::cuda::NetConfig c;
+    const std::string model = get("model", "gsrc");
+    if (model == "gsrc") c.mode = gsr::cuda::Mode::GsrC;
+    else if (model == "gsr") c.mode = gsr::cuda::Mode::Alg12;
+    else if (model == "baseline") c.mode = gsr::cuda::Mode::Rev;
+    else throw gsr::ConfigError("--model must be gsrc, gsr or baseline");
+    c.layers = std::stoi(get("layers", "8"));
+    c.hidden = std::stoi(get("hidden", "64"));
+    c.groups = std::stoi(get("groups", "2"));
+    c.k = std::stoi(get("k", "8"));
+    const std::string prec = get("precision", "fp32");
+    if (prec != "fp32" && prec != "tf32") throw gsr::ConfigError("--precision must be fp32 or tf32");
+    c.precision = prec == "tf32" ? gsr::cuda::Precision::Tf32 : gsr::cuda::Precision::Fp32;
+    const std::string norm_s = get("norm", "row_mean");
+    gsr::cuda::Norm norm = gsr::cuda::Norm::RowMean;
+    if (norm_s == "none") norm = gsr::cuda::Norm::None;
+    else if (norm_s == "sym") norm = gsr::cuda::Norm::SymDegree;
+    else if (norm_s != "row_mean") throw gsr::ConfigError("--norm must be none, row_mean or sym");
+    const int epochs = std::stoi(get("epochs", "5"));
+    gsr::cuda::OptimConfig opt;
+    opt.lr = std::stof(get("lr", "1e-3"));
+
+    const Graph g = read_gsrg(a["graph"]);
+    const Nodes d = read_gsrn(a["nodes"]);
+    if (d.n != g.n) throw gsr::ShapeError("node file n != graph n");
+    c.d_in = static_cast<int>(d.d_in);
+
+    gsr::cuda::Context ctx(std::stoi(get("device", "0")));
+    ctx.upload_graph(g.n, g.row_ptr, g.col_idx, norm);
+    ctx.init_model(c);
+    const index_t P = ctx.num_params();
+    std::vector<float> p;
+    if (a.count("params")) {
+        const auto b = slurp(a["params"]);
+        if (b.size() != 4 * static_cast<size_t>(P)) throw gsr::ShapeError("--params: expected " + std::to_string(P) + " f32 values");
+        p.resize(static_cast<size_t>(P));
+        std::memcpy(p.data(), b.data(), b.size());
+    } else {
+        p = init_params(c, P, std::stoull(get("seed", "0")));
+    }
+    ctx.set_params(p);
+    ctx.upload_data(d.x.data(), d.y.data(), d.train.data());
+    ctx.set_graph_capture(true);
+
+    std::ofstream rep;
+    std::ostream* out = &std::cout;
+    if (a.count("report")) {
+        rep.open(a["report"]);
+        if (!rep) throw gsr::ResourceError("cannot open report " + a["report"]);
+        out = &rep;
+    }
+    double total = 0.0, first = 0.0, last = 0.0;
+    for (int ep = 0; ep < epochs; ++ep) {
+        if (ep == 1) ctx.high_water_reset();  // warmup epoch excluded
+        last = ctx.train_step(opt);
+        if (ep == 0) first = last;
+        if (!std::isfinite(last)) throw std::runtime_error("loss is not finite at epoch " + std::to_string(ep));
+        const gsrc_timing t = ctx.last_timing();
+        const gsrc_mem_report m = ctx.memory();
+        if (ep > 0) total += t.t_total;
+        std::ostringstream s;
+        s.precision(9);
+        s << "{\"record\":\"epoch\",\"epoch\":" << ep << ",\"train_loss\":" << last << ",\"t_total\":" << t.t_total
+          << ",\"peak_active_bytes\":" << m.peak_active_bytes << ",\"reserved_bytes\":" << m.reserved_bytes
+          << ",\"utilization\":" << m.utilization << "}\n";
+        *out << s.str();
+    }
+    const gsrc_mem_report m = ctx.memory();
+    std::ostringstream s;
+    s.precision(9);
+    s << "{\"record\":\"summary\",\"version\":\"" << gsr::kArtifactVersion << "\",\"model\":\"" << model << "\",\"n\":" << g.n
+      << ",\"e\":" << g.col_idx.size() << ",\"layers\":" << c.layers << ",\"hidden\":" << c.hidden << ",\"groups\":" << c.groups
+      << ",\"k\":" << c.k << ",\"params\":" << P << ",\"epochs\":" << epochs << ",\"first_loss\":" << first << ",\"last_loss\":" << last
+      << ",\"steps_per_s\":" << (epochs > 1 && total > 0 ? (epochs - 1) / total : 0.0) << ",\"peak_active_bytes\":" << m.peak_active_bytes
+      << ",\"kernel_launches\":" << ctx.kernel_launches() << "}\n";
+    *out << s.str();
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    // Exit codes: 0 ok, 1 validation, 3 resource.
+    try {
+        return run(argc, argv);
+    } catch (const gsr::ConfigError& e) {
+        std::cerr << "config error: " << e.what() << "\n";
+        return 1;
+    } catch (const gsr::ResourceError& e) {
+        std::cerr << "resource error: " << e.what() << "\n";
+        return 3;
+    } catch (const std::invalid_argument& e) {
+        std::cerr << "config error: bad numeric flag value (" << e.what() << ")\n";
+        return 1;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 2;
+    }
+}
