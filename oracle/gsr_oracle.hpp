@@ -302,22 +302,40 @@ void spmm_sparse(const Graph& g, bool transpose, int w, int k, const T* vals, co
     work().rows_touched += static_cast<std::uint64_t>(g.n);
 }
 
+// TF32 transform mode (the device's tcgen05 kind::tf32 path, GSRC_GEMM_TF32):
+// both operands of every block transform are rounded to TF32 (10-bit
+// mantissa, round-to-nearest ties-away, = PTX cvt.rna.tf32.f32, which the
+// kernel applies when it stages the UMMA operands). Products of two TF32
+// values are exact in FP32, so this oracle and the tensor core then differ
+// only by the accumulation order of w exact products.
+inline bool& tf32_transform() { static bool v = false; return v; }
+inline float tf32_rna(float x) {
+    std::uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+    std::memcpy(&x, &u, 4);
+    return x;
+}
+inline double tf32_rna(double x) { return static_cast<double>(tf32_rna(static_cast<float>(x))); }
+
 // One row of a dense transform: out[j] = fma-chain_m a[m]*B(m,j) (+0 start).
 // B(m,j) = b[m*ldb + j] (plain) or b[j*ldb + m] (transposed operand).
+// rnd: TF32 operand rounding (see tf32_transform).
 template <typename T>
-inline void gemm_row(const T* a, int K, int N, const T* b, index_t ldb, bool bt, T* out) {
+inline void gemm_row(const T* a, int K, int N, const T* b, index_t ldb, bool bt, T* out, bool rnd = false) {
     T acc[1024];
     for (int j = 0; j < N; ++j) acc[j] = T(0);
+    auto B = [&](T v) { return rnd ? static_cast<T>(tf32_rna(v)) : v; };
     if (!bt) {
         for (int m = 0; m < K; ++m) {
-            const T am = a[m];
+            const T am = B(a[m]);
             const T* brow = b + m * ldb;
-            for (int j = 0; j < N; ++j) acc[j] = std::fma(am, brow[j], acc[j]);
+            for (int j = 0; j < N; ++j) acc[j] = std::fma(am, B(brow[j]), acc[j]);
         }
     } else {
         for (int m = 0; m < K; ++m) {
-            const T am = a[m];
-            for (int j = 0; j < N; ++j) acc[j] = std::fma(am, b[j * ldb + m], acc[j]);
+            const T am = B(a[m]);
+            for (int j = 0; j < N; ++j) acc[j] = std::fma(am, B(b[j * ldb + m]), acc[j]);
         }
     }
     for (int j = 0; j < N; ++j) out[j] = acc[j];
@@ -325,11 +343,12 @@ inline void gemm_row(const T* a, int K, int N, const T* b, index_t ldb, bool bt,
 
 // gemm: out = a·b (+= when accumulate); WorkCounter += M·K·N.
 template <typename T>
-void gemm(index_t M, int K, int N, const T* a, index_t lda, const T* b, index_t ldb, bool bt, bool accumulate, T* out, index_t ldo) {
+void gemm(index_t M, int K, int N, const T* a, index_t lda, const T* b, index_t ldb, bool bt, bool accumulate, T* out, index_t ldo,
+          bool rnd = false) {
     pfor(M, [&](index_t bg, index_t en) {
         T tmp[1024];
         for (index_t r = bg; r < en; ++r) {
-            gemm_row(a + r * lda, K, N, b, ldb, bt, tmp);
+            gemm_row(a + r * lda, K, N, b, ldb, bt, tmp, rnd);
             T* o = out + r * ldo;
             for (int j = 0; j < N; ++j) o[j] = accumulate ? o[j] + tmp[j] : tmp[j];
         }
@@ -357,7 +376,7 @@ enum Epi : int {
 // gsr_forward_block / dense_block, aggregate-then-transform SPEC.md:286).
 template <typename T>
 inline void transform_row(const T* z, int w, const T* W, const T* bias, BlockFlags f, T* h) {
-    if (f.use_weight) gemm_row(z, w, w, W, w, false, h);
+    if (f.use_weight) gemm_row(z, w, w, W, w, false, h, tf32_transform());
     else for (int j = 0; j < w; ++j) h[j] = z[j];
     if (f.use_bias) for (int j = 0; j < w; ++j) h[j] = h[j] + bias[j];
 }
@@ -460,7 +479,7 @@ void gsr_backward_block(const Graph& g, int w, int k, const T* m, index_t ldm, c
                         const std::int32_t* fidx, const T* W, BlockFlags f, T* out, index_t ldo, T* dW, T* db) {
     const index_t n = g.n;
     std::vector<T> tm(static_cast<size_t>(n) * w), vg(static_cast<size_t>(n) * k);
-    if (f.use_weight) gemm<T>(n, w, w, m, ldm, W, w, true, false, tm.data(), w);
+    if (f.use_weight) gemm<T>(n, w, w, m, ldm, W, w, true, false, tm.data(), w, tf32_transform());
     else pfor(n, [&](index_t b, index_t e) { for (index_t r = b; r < e; ++r) for (int j = 0; j < w; ++j) tm[r * w + j] = m[r * ldm + j]; });
     gather<T>(n, w, k, tm.data(), w, isrc, vg.data());
     spmm_sparse<T>(g, true, w, k, vg.data(), isrc, out, ldo);
@@ -658,8 +677,10 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
         T* Gi = G + i * w;
         if (f.use_weight) {
             std::vector<double> acc;
-            reduce_outer<T>(n, w, w, [&](index_t r, T* x) { std::memcpy(x, Z.data() + r * w, sizeof(T) * w); },
-                            [&](index_t r, T* x) { std::memcpy(x, Gi + r * D, sizeof(T) * w); }, acc);
+            // TF32 mode: dW = tf32(Z)ᵀ·tf32(G_i), the operands the device's dW tensor-core MMA consumes
+            const bool rz = tf32_transform();
+            reduce_outer<T>(n, w, w, [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_rna(Z[r * w + j])) : Z[r * w + j]; },
+                            [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_rna(Gi[r * D + j])) : Gi[r * D + j]; }, acc);
             T* dw = net.dW(l, i);
             for (int q = 0; q < w * w; ++q) dw[q] = static_cast<T>(static_cast<double>(dw[q]) + acc[q]);
         }
@@ -674,7 +695,7 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
             T yt[1024], t[1024];
             for (index_t r = b; r < e; ++r) {
                 spmm_row(bwd, r, w, Gi, D, yt);
-                if (f.use_weight) gemm_row(yt, w, w, net.W(l, i), w, true, t);
+                if (f.use_weight) gemm_row(yt, w, w, net.W(l, i), w, true, t, tf32_transform());
                 else for (int j = 0; j < w; ++j) t[j] = yt[j];
                 auto add_to = [&](T* dst) {
                     if (rev) {

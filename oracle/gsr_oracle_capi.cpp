@@ -181,6 +181,11 @@ extern "C" {
 
 const char* gsro_last_error() { return g_err.c_str(); }
 
+int gsro_set_tf32(int on) {
+    gsro::tf32_transform() = on != 0;
+    return 0;
+}
+
 int gsro_set_threads(int n) {
     return guarded([&] {
         pool_ref() = nullptr;

@@ -64,6 +64,12 @@ def _sfx(dtype):
     return "f64" if np.dtype(dtype) == np.float64 else "f32"
 
 
+def set_tf32(on):
+    """TF32 transform mode: round both operands of every block transform to TF32
+    (cvt.rna), as the device's tcgen05 kind::tf32 path stages them."""
+    _chk(lib().gsro_set_tf32(int(bool(on))))
+
+
 def set_threads(n):
     _chk(lib().gsro_set_threads(int(n)))
 

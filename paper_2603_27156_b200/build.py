@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libgsrcuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-SOURCES = ["kernels.cu", "tile_w32.cu", "tile_w64.cu", "tile_w128.cu", "capi.cu"]
+SOURCES = ["kernels.cu", "tile_w32.cu", "tile_w64.cu", "tile_w128.cu", "fast.cu", "capi.cu"]
 HEADERS = ["kernels.cuh", "common.cuh", "tile.cuh", os.path.join(ROOT, "include", "gsr_cuda.h")]
 
 

@@ -119,6 +119,8 @@ struct gsrc_ctx {
     int norm = 0;
     int *rp = nullptr, *ci = nullptr, *trp = nullptr, *tci = nullptr;
     float *row_f = nullptr, *col_f = nullptr;
+    int *hub_f = nullptr, *hub_b = nullptr;   // rows with > kSeg edges (fwd CSR / transpose), fast path
+    int nhub_f = 0, nhub_b = 0;
     size_t graph_bytes = 0;
 
     // persistent: model state
@@ -140,7 +142,7 @@ struct gsrc_ctx {
 
     // activation arena
     Arena arena;
-    float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr;
+    float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr, *Zh = nullptr;
     uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
     std::vector<uint8_t*> c1, c2;
     std::vector<char> filled;
@@ -163,7 +165,7 @@ struct gsrc_ctx {
     ~gsrc_ctx() {
         if (g_fb) cudaGraphExecDestroy(g_fb);
         if (g_step) cudaGraphExecDestroy(g_step);
-        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)params, (void*)grads,
+        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
@@ -239,6 +241,73 @@ struct gsrc_ctx {
         ++launches;
     }
 
+    // ---- thread-per-row tcgen05 fast path (fast.cu): GSR-C in TF32 mode ------
+    bool fast() const { return cfg.mode == GSRC_MODE_GSRC && cfg.gemm == GSRC_GEMM_TF32 && fast_supported(w, k); }
+    FastArgs fast_base(bool transpose) const {
+        FastArgs f;
+        f.n = static_cast<int>(n);
+        f.w = w;
+        f.ld = ld;
+        f.k = k;
+        f.dir = transpose ? bwd() : fwd();
+        f.Zh = Zh;
+        return f;
+    }
+    void run_hub(bool sparse, const FastArgs& f, bool transpose) {
+        const int nh = transpose ? nhub_b : nhub_f;
+        if (!nh) return;
+        CK(launch_hub(sparse, f, transpose ? hub_b : hub_f, nh, stream));
+        ++launches;
+    }
+    void run_fast(int kind, const FastArgs& f) {
+        CK(launch_fast(kind, f, stream, &last_grid));
+        ++launches;
+    }
+    // f_i with Eq. 6 add (+ GS of the output for the next block)
+    void fast_block_forward(int l, int i, const uint8_t* rec, uint8_t* gs_out) {
+        FastArgs f = fast_base(false);
+        f.rec_in = rec;
+        run_hub(true, f, false);
+        f.Wm = Wb(l, i);
+        f.bias = Bb(l, i);
+        f.R = plane(X, i);
+        f.out = plane(X, i);
+        f.gs_out = gs_out;
+        f.k_gs = k;
+        run_fast(0, f);
+    }
+    // Eq. 7 inverse of block i + dW/db, then the masked input gradient
+    void fast_block_backward(int l, int i, const uint8_t* rec) {
+        fast_inverse(l, i, rec);
+        reduce_block_grads(l, i);
+        fast_input_grad(l, i, rec);
+    }
+    void fast_inverse(int l, int i, const uint8_t* rec) {
+        FastArgs f = fast_base(false);
+        f.rec_in = rec;
+        run_hub(true, f, false);
+        f.Wm = Wb(l, i);
+        f.bias = Bb(l, i);
+        f.R = plane(X, i);
+        f.out = plane(X, i);
+        f.G = plane(G, i);
+        f.part = part;
+        f.want_db = cfg.use_bias;
+        run_fast(1, f);
+    }
+    void fast_input_grad(int l, int i, const uint8_t* rec) {
+        FastArgs b = fast_base(true);
+        b.x_in = plane(G, i);
+        run_hub(false, b, true);
+        b.Wm = Wb(l, i);
+        b.gemm_t = 1;
+        b.mrec = rec;
+        b.k_m = k;
+        if (i > 0) { b.dst[0] = plane(G, i - 1); b.ndst = 1; }
+        else { for (int p = 1; p < C; ++p) b.dst[p - 1] = plane(G, p); b.ndst = C - 1; }
+        run_fast(2, b);
+    }
+
     // ---- GSR-C / REV layers ---------------------------------------------------
     void rev_layer_forward(int l) {
         const bool sparse = cfg.mode == GSRC_MODE_GSRC;
@@ -246,6 +315,13 @@ struct gsrc_ctx {
         uint8_t* nxt = recB;
         if (sparse) run_gs_groupsum(X, cur);
         else run_sum_planes(X, U);
+        if (fast() && cfg.use_weight) {
+            for (int i = 0; i < C; ++i) {
+                fast_block_forward(l, i, cur, i + 1 < C ? nxt : nullptr);
+                std::swap(cur, nxt);
+            }
+            return;
+        }
         for (int i = 0; i < C; ++i) {
             TileArgs a = tile_base();
             a.dir = fwd();
@@ -278,6 +354,10 @@ struct gsrc_ctx {
         } else {
             if (i > 0) u = plane(X, i - 1);
             else { run_sum_planes(X, U); u = U; }
+        }
+        if (fast() && cfg.use_weight && with_grads) {
+            fast_block_backward(l, i, recA);
+            return;
         }
         TileArgs a = tile_base();
         a.dir = fwd();
@@ -443,6 +523,7 @@ struct gsrc_ctx {
         total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
         if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
+        if (fast()) total += bytes_rounded(pl * sizeof(float));            // Zh (hub-row aggregates)
         if (alg12) total += 2 * bytes_rounded(pl * sizeof(float)) + 3 * bytes_rounded(rb) + 2 * static_cast<size_t>(cfg.layers) * bytes_rounded(rb);
         arena.plan(total);
         X = arena.lease<float>(pl * C);
@@ -456,6 +537,7 @@ struct gsrc_ctx {
         loss_dev = arena.lease<double>(1);
         U = nullptr;
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
+        Zh = fast() ? arena.lease<float>(pl) : nullptr;
         c1.clear();
         c2.clear();
         if (alg12) {
@@ -623,6 +705,7 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         }
         CK(cudaStreamSynchronize(ctx->stream));
         for (void* p : {(void*)ctx->rp, (void*)ctx->ci, (void*)ctx->trp, (void*)ctx->tci, (void*)ctx->row_f, (void*)ctx->col_f}) if (p) cudaFree(p);
+        ctx->rp = ctx->ci = ctx->trp = ctx->tci = nullptr;
         ctx->graph_bytes = 0;
         ctx->rp = dmalloc<int>(n + 1, &ctx->graph_bytes);
         ctx->ci = dmalloc<int>(e, &ctx->graph_bytes);
@@ -636,6 +719,19 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         if (e) CK(cudaMemcpy(ctx->tci, tci.data(), sizeof(int) * e, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->row_f, rf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->col_f, cf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        // rows longer than one aggregation segment, per direction (fast path hubs)
+        std::vector<int> hf, hb;
+        for (int64_t r = 0; r < n; ++r) {
+            if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
+            if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
+        }
+        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b}) if (p) cudaFree(p);
+        ctx->nhub_f = static_cast<int>(hf.size());
+        ctx->nhub_b = static_cast<int>(hb.size());
+        ctx->hub_f = dmalloc<int>(hf.size(), &ctx->graph_bytes);
+        ctx->hub_b = dmalloc<int>(hb.size(), &ctx->graph_bytes);
+        if (!hf.empty()) CK(cudaMemcpy(ctx->hub_f, hf.data(), sizeof(int) * hf.size(), cudaMemcpyHostToDevice));
+        if (!hb.empty()) CK(cudaMemcpy(ctx->hub_b, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
         CK(cudaDeviceSynchronize());  // pageable copies may still be in flight when cudaMemcpy returns
         const bool resize = ctx->n != n;
         ctx->n = n;
@@ -1123,17 +1219,24 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
             CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
             return static_cast<double>(ms) / reps;
         };
+        if (ctx->fast() && ctx->cfg.use_weight) {
+            // the three fast-path block kernels (each with its hub-row pre-pass) at layer 0, block 1
+            out[0] = time_it([&] { ctx->fast_block_forward(l, 1, ctx->recA, ctx->recB); });
+            out[4] = time_it([&] { ctx->fast_inverse(l, 1, ctx->recA); });
+            out[8] = time_it([&] { ctx->fast_input_grad(l, 1, ctx->recA); });
+        }
         TileArgs fa = ctx->tile_base();
         fa.agg = AGG_SPARSE; fa.dir = ctx->fwd(); fa.rec_in = ctx->recA; fa.k_in = ctx->k;
         fa.gemm = ctx->cfg.use_weight ? GEMM_W : GEMM_NONE; fa.Wm = ctx->Wb(l, 1); fa.bias = ctx->Bb(l, 1);
         fa.epi = EPI_ADD; fa.R = ctx->plane(ctx->X, 1); fa.out = ctx->plane(ctx->X, 1); fa.gs_out = ctx->recB; fa.k_gs = ctx->k;
-        out[0] = time_it([&] { ctx->run_tile(fa); });
+        const bool fp = ctx->fast() && ctx->cfg.use_weight;
+        if (!fp) out[0] = time_it([&] { ctx->run_tile(fa); });
         out[1] = csr + 2 * n * rb + 8 * n * w;
         out[2] = L * C;
         out[3] = 2 * n * w * w;
         TileArgs ra = fa;
         ra.epi = EPI_SUB; ra.gs_out = nullptr; ra.G = ctx->plane(ctx->G, 1); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
-        out[4] = time_it([&] { ctx->run_tile(ra); });
+        if (!fp) out[4] = time_it([&] { ctx->run_tile(ra); });
         out[5] = csr + n * rb + 12 * n * w;
         out[6] = L * C;
         out[7] = 4 * n * w * w;
@@ -1141,7 +1244,7 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         ba.agg = AGG_DENSE; ba.dir = ctx->bwd(); ba.x_in = ctx->plane(ctx->G, 1);
         ba.gemm = ctx->cfg.use_weight ? GEMM_WT : GEMM_NONE; ba.Wm = ctx->Wb(l, 1);
         ba.epi = EPI_MASKED_ADD; ba.rrec = ctx->recA; ba.k_r = ctx->k; ba.dst[0] = ctx->plane(ctx->G, 0); ba.ndst = 1;
-        out[8] = time_it([&] { ctx->run_tile(ba); });
+        if (!fp) out[8] = time_it([&] { ctx->run_tile(ba); });
         out[9] = csr + 4 * n * w + n * rb + 8 * n * k;
         out[10] = L * C;
         out[11] = 2 * n * w * w;

@@ -1,0 +1,686 @@
+// Thread-per-row tcgen05 kernels for the GSR-C training step in TF32 mode.
+//
+// The GSR-C step (Eq. 6-7 grouped reversible layers with GS-sparse blocks,
+// SURVEY.md §8a rows a20-a22/a33) runs three block shapes, 3 × C × L launches
+// per step. k_tile (tile.cuh) implements every shape generically; these are
+// the lean sm_100a versions of the three the bench step actually runs:
+//
+//   FWD  y'_i = x_i + (Â·scatter(V,I))·W_i + b_i, then GS_k(y'_i) → records
+//        (gsr_forward_block SPEC.md:253-261 + Eq. 6 add + gs_topk SPEC.md:67-76)
+//   INV  x_i = y'_i − (Â·scatter(V,I))·W_i − b_i   (Eq. 7)
+//        + dW_i += Zᵀ·G_i on the tensor core (db_i += colsum G_i)
+//   BIN  dst_p[r, I[r]] += ((Âᵀ·G_i)·W_iᵀ)[r, I[r]]  (exact GS-masked input
+//        gradient, SPEC.md:262-270 restated for Eq. 6-7)
+//
+// Design (one CTA = 128 threads = one 128-row tile at a time, persistent):
+//   * thread t owns tile row t end to end: it walks its CSR edges (≤ kSeg;
+//     longer "hub" rows come pre-aggregated from k_hub_* in the oracle's
+//     canonical segment order), accumulates straight into its row of the UMMA
+//     A operand in shared memory (K-major SWIZZLE_128B), scales and rounds it
+//     to TF32, reads its accumulator row back from TMEM (warp w ↔ lane
+//     quadrant w), and runs its row's epilogue and GS top-k alone — no
+//     cross-thread exchange, so the only CTA barriers are around the MMA;
+//   * the residual / gradient row tiles are staged with cp.async (LDGSTS)
+//     into swizzled shared memory while the aggregation runs;
+//   * one elected thread issues tcgen05.mma kind::tf32 (M = 128, N = W) and,
+//     for INV, a second MN-major MMA accumulating dW = Zᵀ·G in TMEM across all
+//     tiles of the CTA (per-CTA partials, reduced in fixed order afterwards).
+// Arithmetic per row is the oracle's (oracle/gsr_oracle.hpp, TF32 mode):
+// canonical segmented aggregation, row scale, cvt.rna TF32 operands.
+#include "tile.cuh"
+
+namespace gsrk {
+namespace fast {
+
+using tile::mbar_init;
+using tile::mbar_wait;
+using tile::smem_u32;
+using tile::tf32_rna;
+using tile::tmem_ld;
+
+constexpr int TR = 128;       // rows per tile == threads per CTA
+constexpr int kSegF = tile::kSeg;
+
+enum Kind : int { FWD = 0, INV = 1, BIN = 2 };
+
+// Swizzled [TR][W] fp32 tile (UMMA SWIZZLE_128B canonical form, K-major for
+// the row-as-M operand, MN-major when rows are K): 32-column regions of
+// TR × 128 B; the 16 B chunk j of row r sits at chunk j ^ (r & 7). A row's
+// float4 chunks hit 8 distinct bank groups across 8 consecutive rows, so
+// thread-per-row LDS/STS.128 are conflict-free.
+__device__ __forceinline__ int zo(int r, int m) { return (m >> 5) * (TR * 32) + r * 32 + ((m ^ ((r & 7) << 2)) & 31); }
+
+// MN-major tf32 operands must use the SWIZZLE_128B_BASE32B canonical layout
+// (32 B granules; granule j of row r at j ^ (r & 3)); rows are the K index.
+__device__ __forceinline__ int zb(int r, int m) { return (m >> 5) * (TR * 32) + r * 32 + ((((m >> 3) & 3) ^ (r & 3)) << 3) + (m & 7); }
+
+// Shared memory (floats; every operand region 1 KB aligned):
+//   FWD: Ws | Zs | St      BIN: Ws | Zs      INV: Ws | Zs | Z2 | Gs
+// Zs is the UMMA A operand; once the MMA has completed it holds the tile's
+// output rows (FWD: for the GS top-k; BIN: h for the masked scatter). St:
+// per-thread CBSR record staging (96 B). Z2 = Z and Gs = G in BASE32B
+// MN-major for dW. The residual row is read straight from global into
+// registers while the MMAs run.
+template <int W>
+struct Plan {
+    static constexpr int ws = W * W;
+    static constexpr int tile = TR * W;
+    // the dW MMA runs with M = 128 (A = Zᵀ: four 32-column atoms at TR·128 B
+    // stride from Z2); rows m ≥ W read past Z2 into Gs and land in TMEM lanes
+    // that are never read, so Z2 + 4 atoms must stay inside the allocation.
+    static constexpr int inv_tail = 2 * tile > 4 * TR * 32 ? 2 * tile : 4 * TR * 32;
+    static constexpr int stage = TR * 24;
+    static constexpr int floats(int kind) { return kind == INV ? ws + tile + inv_tail : (kind == FWD ? ws + tile + stage : ws + tile); }
+    static constexpr size_t bytes(int kind) { return static_cast<size_t>(floats(kind) + 64) * sizeof(float); }
+};
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Stage rows [row0, row0 + TR) of an n × ld plane into a swizzled smem tile
+// (columns ≥ ld zero-filled), coalesced 16 B chunks.
+template <int W, bool B32>
+__device__ __forceinline__ void stage_tile(float* dst, const float* src, int row0, int n, int ld) {
+    constexpr int CPR = W / 4;
+    for (int i = threadIdx.x; i < TR * CPR; i += TR) {
+        const int r = i / CPR, c = (i % CPR) * 4;
+        const bool ok = row0 + r < n && c < ld;
+        const float* g = ok ? src + static_cast<size_t>(row0 + r) * ld + c : src;
+        cp_async16(dst + (B32 ? zb(r, c) : zo(r, c)), g, ok ? 16 : 0);
+    }
+    cp_async_commit();
+}
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+    return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+// MN-major SWIZZLE_128B_BASE32B (layout type 1): LBO = 32-column atom stride
+// (TR·128 B), SBO = 4-row group stride (512 B).
+__device__ __forceinline__ uint64_t desc_mn32(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>((TR * 128) >> 4) << 16) | (static_cast<uint64_t>(512 >> 4) << 32) |
+           (1ull << 46) | (1ull << 61);
+}
+
+// kind::tf32, D = F32, M = 128, N = W; a/b major: 0 = K, 1 = MN.
+template <int N>
+__host__ __device__ constexpr uint32_t idesc(int a_mn, int b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(TR >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) { tile::umma_tf32(d, a, b, id, acc); }
+
+// ---- sparse row aggregation (regular rows, deg ≤ kSeg) ----------------------
+// z[m] += sc · v over the row's edges in CSR order, the k (index, value)
+// pairs of each record in slot order — the oracle's spmm_sparse_row order.
+template <int W>
+__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
+    const int k = a.k;
+    const int RB = rec_bytes(k), nv4 = (k + 3) >> 2;
+    const bool unit = a.dir.unit_edge != 0;
+    int cs[kSegF];
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + e0 + u) : 0;
+    float sc[kSegF];
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) sc[u] = (!unit && u < ne) ? __ldg(a.dir.edge_f + cs[u]) : 1.f;
+    const int rbase = r * 32, rx = (r & 7) << 2;
+#pragma unroll
+    for (int u = 1; u < kSegF; ++u)  // later records toward L2 while the first ones load
+        if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
+    tile::SparseRec buf[2];
+    if (ne > 0) tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) {
+        if (u < ne) {
+            if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
+            const tile::SparseRec& rc = buf[u & 1];
+            const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
+            const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
+                                  rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
+            // a record's k indices are distinct: load all k accumulators, add,
+            // store (no read-after-write chain inside a record)
+            float* zp[16];
+            float old[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int m = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                zp[j] = Zs + rbase + ((m ^ rx) & 31) + (m >> 5) * (TR * 32);
+                if (j < k) old[j] = *zp[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < k) *zp[j] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc[u], vv[j]));
+        }
+    }
+}
+
+// ---- dense row aggregation (regular rows): z = Σ_e sc_e · x[c_e], in CSR order
+template <int W>
+__device__ __forceinline__ void agg_dense_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
+    const bool unit = a.dir.unit_edge != 0;
+    int cs[kSegF];
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + e0 + u) : 0;
+    float sc[kSegF];
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) sc[u] = (!unit && u < ne) ? __ldg(a.dir.edge_f + cs[u]) : 1.f;
+    constexpr int CH = 8;  // columns per pass: ne × 2 float4 loads in flight
+#pragma unroll 1
+    for (int c0 = 0; c0 < W; c0 += CH) {
+        float4 v[kSegF][CH / 4];
+#pragma unroll
+        for (int u = 0; u < kSegF; ++u)
+#pragma unroll
+            for (int q = 0; q < CH / 4; ++q)
+                v[u][q] = (u < ne && c0 + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(cs[u]) * a.ld + c0 + 4 * q)
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        float acc[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) acc[q] = 0.f;
+#pragma unroll
+        for (int u = 0; u < kSegF; ++u) {
+            if (u < ne) {
+#pragma unroll
+                for (int q = 0; q < CH / 4; ++q) {
+                    const float x[4] = {v[u][q].x, v[u][q].y, v[u][q].z, v[u][q].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc[4 * q + t] = __fadd_rn(acc[4 * q + t], unit ? x[t] : __fmul_rn(sc[u], x[t]));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH / 4; ++q)
+            *reinterpret_cast<float4*>(Zs + zo(r, c0 + 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    }
+}
+
+// GS top-k of a row held in a swizzled smem tile → CBSR record.
+// Same selection as dev::gs_select_row: k-th largest magnitude key T via a
+// bitonic top-G tree, then columns ascending, ties at T lowest column first.
+template <int W, int G>
+__device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* stage, uint8_t* rec_out) {
+    uint32_t s[W];
+#pragma unroll
+    for (int c = 0; c < W; c += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(Ts + zo(r, c));
+        s[c] = c < w ? dev::mag_key(v.x) : 0u;
+        s[c + 1] = c + 1 < w ? dev::mag_key(v.y) : 0u;
+        s[c + 2] = c + 2 < w ? dev::mag_key(v.z) : 0u;
+        s[c + 3] = c + 3 < w ? dev::mag_key(v.w) : 0u;
+    }
+    // bitonic sort of every G-key group (descending), all indices compile-time
+    constexpr int LG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
+    static_assert((1 << LG) == G, "G must be a power of two <= 16");
+    constexpr int LW = W == 128 ? 7 : (W == 64 ? 6 : (W == 32 ? 5 : 0));
+    static_assert((1 << LW) == W, "W must be 32 or 64");
+#pragma unroll
+    for (int ls = 1; ls <= LG; ++ls) {
+        const int size = 1 << ls;
+#pragma unroll
+        for (int lt = ls - 1; lt >= 0; --lt) {
+            const int stride = 1 << lt;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const uint32_t x = s[i], y = s[j];
+                    const uint32_t hi = max(x, y), lo = min(x, y);
+                    if (((i % G) & size) == 0) { s[i] = hi; s[j] = lo; }
+                    else { s[i] = lo; s[j] = hi; }
+                }
+            }
+        }
+    }
+    // merge tree: top-G of groups (g, g + span) → group g, sorted
+#pragma unroll
+    for (int lsp = LG; lsp < LW; ++lsp) {
+        const int span = 1 << lsp;
+#pragma unroll
+        for (int g = 0; g < W; g += 2 * span) {
+#pragma unroll
+            for (int i = 0; i < G; ++i) s[g + i] = max(s[g + i], s[g + span + G - 1 - i]);
+#pragma unroll
+            for (int lt = LG - 1; lt >= 0; --lt) {
+                const int stride = 1 << lt;
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const uint32_t x = s[g + i], y = s[g + j];
+                        s[g + i] = max(x, y);
+                        s[g + j] = min(x, y);
+                    }
+                }
+            }
+        }
+    }
+    // T = s[k-1] = min of the first k (descending); a select chain here would
+    // be folded into a dynamically indexed (local-memory) load
+    uint32_t T = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < G; ++i) T = min(T, i < k ? s[i] : 0xffffffffu);
+    int gt = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) gt += s[i] > T;
+    int take = k - gt;
+    const int KH = rec_kh(k);
+    int slot = 0;
+    float* rv = reinterpret_cast<float*>(stage + KH);
+#pragma unroll
+    for (int c = 0; c < W; c += 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int col = c + t;
+            const uint32_t key = col < w ? dev::mag_key(vv[t]) : 0u;
+            const bool eq = key == T && col < w;
+            const bool pick = key > T || (eq && take > 0);
+            take -= (eq && take > 0) ? 1 : 0;
+            if (pick) {
+                stage[slot] = static_cast<uint8_t>(col);
+                rv[slot] = vv[t];
+                ++slot;
+            }
+        }
+    }
+    const int RB = rec_bytes(k);
+    for (int b = 0; b < RB; b += 16) *reinterpret_cast<uint4*>(rec_out + b) = *reinterpret_cast<const uint4*>(stage + b);
+}
+
+template <int W, int KIND>
+__global__ void __launch_bounds__(TR, 1) k_fast(FastArgs a) {
+    using Pl = Plan<W>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* base = reinterpret_cast<float*>(smem_raw);
+    if ((smem_u32(base) & 1023u) != 0) __trap();  // UMMA SW128 atoms need 1 KB alignment
+    float* Ws = base;
+    float* Zs = Ws + Pl::ws;
+    float* St = Zs + Pl::tile;   // FWD
+    float* Z2 = Zs + Pl::tile;   // INV
+    float* Gs = Z2 + Pl::tile;   // INV
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(KIND));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+
+    const int t = threadIdx.x, wid = t >> 5;
+    const int n_tiles = (a.n + TR - 1) / TR;
+    constexpr uint32_t TCOLS = KIND == INV ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+
+    // transform operand Bᵀ[n][m] (K-major SW128, region stride W·32), TF32-rounded
+    for (int i = t; i < W * W; i += TR) {
+        const int r = i / W, c = i % W;  // contraction index r, output column c
+        float v = 0.f;
+        if (r < a.w && c < a.w) v = a.gemm_t ? a.Wm[c * a.w + r] : a.Wm[r * a.w + c];
+        Ws[tile::boff<W>(c, r)] = tf32_rna(v);
+    }
+    if (t == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
+    if (wid == 0) tile::tmem_alloc(tslot, TCOLS);
+    tile::fence_proxy_async();
+    tile::tc_fence_before();
+    __syncthreads();
+    tile::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tlane = static_cast<uint32_t>(32 * wid) << 16;
+    uint32_t ph0 = 0, ph1 = 0;
+    bool dw_pending = false;
+    double dbsum = 0.0;
+
+    for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
+        const int row0 = tile_i * TR;
+        const int row = row0 + t;
+        const bool valid = row < a.n;
+        if (KIND == INV && dw_pending) {  // previous dW MMA still reads Zs / Gs
+            mbar_wait(&bar[1], ph1);
+            ph1 ^= 1u;
+            tile::tc_fence_after();
+            dw_pending = false;
+        }
+        // stage the residual (FWD / INV) and gradient (INV) rows
+        if (KIND == INV) stage_tile<W, true>(Gs, a.G, row0, a.n, a.ld);
+
+        // residual row toward L2 now; it is loaded into registers while the MMA runs
+        if (KIND != BIN && valid && row0 + TR <= a.n) prefetch_l2_bulk(a.R + static_cast<size_t>(row) * a.ld, a.ld * 4);
+        // ---- aggregation into this thread's row of the A operand
+        {
+            const int rbase = t * 32, rx = (t & 7) << 2;
+#pragma unroll
+            for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Zs + rbase + ((c ^ rx) & 31) + (c >> 5) * (TR * 32)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            float rf = 0.f;
+            if (valid) {
+                const int e0 = __ldg(a.dir.ptr + row), e1 = __ldg(a.dir.ptr + row + 1);
+                rf = __ldg(a.dir.out_f + row);
+                const int ne = e1 - e0;
+                if (ne > kSegF) {  // hub row: canonical segmented sum precomputed by k_hub_*
+                    const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
+#pragma unroll
+                    for (int c = 0; c < W; c += 4)
+                        if (c < a.ld) *reinterpret_cast<float4*>(Zs + zo(t, c)) = dev::ld4(zh + c);
+                } else if (KIND == BIN) {
+                    agg_dense_row<W>(a, e0, ne, Zs, t);
+                } else {
+                    agg_sparse_row<W>(a, e0, ne, Zs, t);
+                }
+            }
+            // Â row scale, then TF32 (the operand the tensor core consumes);
+            // INV also keeps the row in the MN-major layout for dW
+#pragma unroll
+            for (int c = 0; c < W; c += 4) {
+                float4* p = reinterpret_cast<float4*>(Zs + zo(t, c));
+                float4 v = *p;
+                v.x = tf32_rna(__fmul_rn(rf, v.x)); v.y = tf32_rna(__fmul_rn(rf, v.y));
+                v.z = tf32_rna(__fmul_rn(rf, v.z)); v.w = tf32_rna(__fmul_rn(rf, v.w));
+                *p = v;
+                if (KIND == INV) *reinterpret_cast<float4*>(Z2 + zb(t, c)) = v;
+            }
+        }
+        if (KIND != BIN) cp_async_wait_all();  // this thread's staged chunks
+        if (KIND == INV) {
+            __syncthreads();  // G rows staged by other threads
+            if (a.want_db && t < a.w) {  // db = colsum(G) in row order, unrounded
+                float s = 0.f;
+                for (int r = 0; r < TR; ++r) s = __fadd_rn(s, Gs[zb(r, t)]);
+                dbsum += static_cast<double>(s);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < W; c += 4) {  // dW's B operand in TF32
+                float4* p = reinterpret_cast<float4*>(Gs + zb(t, c));
+                float4 v = *p;
+                if (!valid) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                v.x = tf32_rna(v.x); v.y = tf32_rna(v.y); v.z = tf32_rna(v.z); v.w = tf32_rna(v.w);
+                *p = v;
+            }
+        }
+        tile::fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
+            tile::tc_fence_after();
+            const uint32_t za = smem_u32(Zs), wa = smem_u32(Ws);
+#pragma unroll
+            for (int kk = 0; kk < W / 8; ++kk)
+                umma(tmem, desc_sw128(za + (kk >> 2) * (TR * 128) + (kk & 3) * 32, 16), desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16),
+                     idesc<W>(0, 0), kk > 0 ? 1u : 0u);
+            tile::umma_commit(&bar[0]);
+            if (KIND == INV) {
+                // dW[m][n] += Σ_r Z[r][m] G[r][n]: A = Zᵀ, B = G, both MN-major
+                // BASE32B (rows = K: 4-row groups at 512 B, 32-col atoms at TR·128 B)
+                const uint32_t z2 = smem_u32(Z2), ga = smem_u32(Gs);
+                const bool first = tile_i == static_cast<int>(blockIdx.x);
+#pragma unroll
+                for (int kk = 0; kk < TR / 8; ++kk)
+                    umma(tmem + W, desc_mn32(z2 + kk * 1024), desc_mn32(ga + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
+                tile::umma_commit(&bar[1]);
+            }
+        }
+        if (KIND == INV) dw_pending = true;
+        float4 Rg[KIND != BIN ? W / 4 : 1];
+        if (KIND != BIN) {  // residual row straight from global while the MMA runs
+#pragma unroll
+            for (int c = 0; c < W; c += 4)
+                Rg[c / 4] = (valid && c < a.ld) ? *reinterpret_cast<const float4*>(a.R + static_cast<size_t>(row) * a.ld + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        mbar_wait(&bar[0], ph0);
+        ph0 ^= 1u;
+        tile::tc_fence_after();
+
+        // ---- epilogue: this thread's accumulator row (TMEM lane = tile row)
+#pragma unroll
+        for (int c0 = 0; c0 < W; c0 += 16) {
+            float h[16];
+            tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(c0), h);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+                const int c = c0 + q;
+                float o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float hv = h[q + j];
+                    if (a.bias) hv = __fadd_rn(hv, c + j < a.w ? __ldg(a.bias + c + j) : 0.f);
+                    o[j] = hv;
+                }
+                float4* rp = reinterpret_cast<float4*>(Zs + zo(t, c));
+                if (KIND != BIN) {
+                    const float4 R = Rg[c / 4];
+                    if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
+                    else { o[0] = __fsub_rn(R.x, o[0]); o[1] = __fsub_rn(R.y, o[1]); o[2] = __fsub_rn(R.z, o[2]); o[3] = __fsub_rn(R.w, o[3]); }
+                    if (valid && c < a.ld) *reinterpret_cast<float4*>(a.out + static_cast<size_t>(row) * a.ld + c) = make_float4(o[0], o[1], o[2], o[3]);
+                }
+                if (KIND != INV) *rp = make_float4(o[0], o[1], o[2], o[3]);  // row kept for GS / masked scatter
+            }
+        }
+        if (KIND == FWD && a.gs_out && valid) {
+            uint8_t* stage = reinterpret_cast<uint8_t*>(St) + t * 96;
+            gs_row<W, 16>(Zs, t, a.w, a.k_gs, stage, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+        }
+        if (KIND == BIN && valid) {
+            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
+            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
+            const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
+            // the mask columns of a row are distinct: all loads first, then the stores
+            int col[16];
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                col[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                if (j < a.k_m) v[j] = Zs[zo(t, col[j])];
+            }
+            for (int p = 0; p < a.ndst; ++p) {
+                float* d = a.dst[p] + static_cast<size_t>(row) * a.ld;
+                float o[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) if (j < a.k_m) o[j] = d[col[j]];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) if (j < a.k_m) d[col[j]] = __fadd_rn(o[j], v[j]);
+            }
+        }
+        tile::tc_fence_before();
+        __syncthreads();
+    }
+    if (KIND == INV) {
+        if (dw_pending) {
+            mbar_wait(&bar[1], ph1);
+            tile::tc_fence_after();
+        }
+        // per-CTA dW partial: TMEM lane m, columns W + n (every CTA writes its slot)
+        const int plen = a.w * a.w + a.w;
+        double* pp = a.part + static_cast<size_t>(blockIdx.x) * plen;
+        const bool any = static_cast<int>(blockIdx.x) < n_tiles;
+#pragma unroll
+        for (int c0 = 0; c0 < W; c0 += 16) {
+            float v[16];
+            tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(W + c0), v);
+            const int m = t;
+            if (m < a.w) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < a.w) pp[m * a.w + c0 + j] = any ? static_cast<double>(v[j]) : 0.0;
+            }
+        }
+        if (t < a.w) pp[a.w * a.w + t] = a.want_db ? dbsum : 0.0;
+    }
+    tile::tc_fence_before();
+    __syncthreads();
+    if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
+}
+
+// ---- hub rows (deg > kSeg): canonical segmented sums, one CTA per row --------
+// Segments of kSeg edges are summed from +0 (thread per segment for records,
+// warp per segment for dense rows) into shared slots, then folded left to
+// right per column — the oracle's aggregation order for long rows.
+template <int W, bool SPARSE>
+__global__ void __launch_bounds__(128) k_hub(FastArgs a, const int* __restrict__ hubs) {
+    constexpr int NS = SPARSE ? (W >= 128 ? 64 : 128) : 16;  // segments per round (static smem ≤ 48 KB)
+    constexpr int PL = W + 4;  // 16 B aligned slot rows
+    __shared__ __align__(16) float P[NS * PL];
+    const int r = __ldg(hubs + blockIdx.x);
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int e0 = __ldg(a.dir.ptr + r), e1 = __ldg(a.dir.ptr + r + 1);
+    const int nseg = (e1 - e0 + kSegF - 1) / kSegF;
+    const bool unit = a.dir.unit_edge != 0;
+    float z = 0.f;  // thread t < W: running fold of column t
+    for (int h0 = 0; h0 < nseg; h0 += NS) {
+        const int nr = min(NS, nseg - h0);
+        if constexpr (SPARSE) {
+            if (t < nr) {
+                float* pr = P + t * PL;
+#pragma unroll
+                for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int lo = e0 + (h0 + t) * kSegF, hi = min(e1, lo + kSegF);
+                const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
+                for (int e = lo; e < hi; ++e) {
+                    const int c = __ldg(a.dir.idx + e);
+                    const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
+                    tile::SparseRec rc;
+                    tile::load_rec16(rc, a.rec_in + static_cast<size_t>(c) * RB, nv4);
+                    const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
+                    const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
+                                          rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
+                    float old[16];
+                    int mm[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        mm[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                        if (j < k) old[j] = pr[mm[j]];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < k) pr[mm[j]] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc, vv[j]));
+                }
+            }
+        } else {
+            constexpr int CPL = W / 32 > 0 ? W / 32 : 1;
+            for (int s = wid; s < nr; s += 4) {
+                const int lo = e0 + (h0 + s) * kSegF, hi = min(e1, lo + kSegF);
+                float acc[CPL];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+                for (int e = lo; e < hi; ++e) {
+                    const int c = __ldg(a.dir.idx + e);
+                    const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int col = lane + 32 * q;
+                        const float x = col < a.ld ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
+                        acc[q] = __fadd_rn(acc[q], unit ? x : __fmul_rn(sc, x));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) if (lane + 32 * q < W) P[s * PL + lane + 32 * q] = acc[q];
+            }
+        }
+        __syncthreads();
+        if (t < W) {
+            int i = 0;
+            if (h0 == 0) { z = P[t]; i = 1; }
+            for (; i + 8 <= nr; i += 8) {  // independent loads, then the ordered fold
+                float pv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pv[q] = P[(i + q) * PL + t];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) z = __fadd_rn(z, pv[q]);
+            }
+            for (; i < nr; ++i) z = __fadd_rn(z, P[i * PL + t]);
+        }
+        __syncthreads();
+    }
+    if (t < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + t] = z;
+}
+
+template <int W, int KIND>
+int occupancy() {
+    static int occ = 0;
+    if (!occ) {
+        int dev = 0, smem_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k_fast<W, KIND>);
+        const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(KIND) + 1024);  // + per-CTA reserved smem
+        const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
+        const int by_regs = 65536 / (regs * TR);
+        constexpr int tcols = KIND == INV ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+        occ = by_smem < by_regs ? by_smem : by_regs;
+        if (occ > 512 / tcols) occ = 512 / tcols;
+        if (occ > 8) occ = 8;
+        if (occ < 1) occ = 1;
+    }
+    return occ;
+}
+
+template <int W, int KIND>
+cudaError_t launch(const FastArgs& a, cudaStream_t s, int* grid_out) {
+    const int tiles = (a.n + TR - 1) / TR;
+    const int cap = tile::sm_count_host() * occupancy<W, KIND>();
+    const int grid = tiles < cap ? tiles : cap;
+    if (grid_out) *grid_out = grid;
+    if (grid == 0) return cudaSuccess;
+    k_fast<W, KIND><<<grid, TR, Plan<W>::bytes(KIND), s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t set_attrs() {
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {cudaFuncSetAttribute(k_fast<W, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(FWD))),
+                          cudaFuncSetAttribute(k_fast<W, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(INV))),
+                          cudaFuncSetAttribute(k_fast<W, BIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
+        if (r != cudaSuccess) e = r;
+    return e;
+}
+
+template <int W>
+cudaError_t launch_w(int kind, const FastArgs& a, cudaStream_t s, int* g) {
+    switch (kind) {
+        case FWD: return launch<W, FWD>(a, s, g);
+        case INV: return launch<W, INV>(a, s, g);
+        default: return launch<W, BIN>(a, s, g);
+    }
+}
+
+template <int W>
+cudaError_t launch_hub_w(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {
+    if (sparse) k_hub<W, true><<<nhub, 128, 0, s>>>(a, hubs);
+    else k_hub<W, false><<<nhub, 128, 0, s>>>(a, hubs);
+    return cudaGetLastError();
+}
+
+}  // namespace fast
+
+// W = 128 would need 256 KB of shared memory for INV: k_tile serves it.
+bool fast_supported(int w, int k) { return w >= 1 && w <= 64 && k >= 1 && k <= 16; }
+
+cudaError_t init_fast_attributes() {
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {fast::set_attrs<32>(), fast::set_attrs<64>()})
+        if (r != cudaSuccess) e = r;
+    return e;
+}
+
+cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out) {
+    if (grid_out) *grid_out = 0;
+    if (a.n == 0) return cudaSuccess;
+    if (kind != fast::BIN && (a.k < 1 || a.k > 16)) return cudaErrorInvalidValue;
+    if (kind == fast::FWD && a.gs_out && (a.k_gs < 1 || a.k_gs > 16)) return cudaErrorInvalidValue;
+    if (a.w <= 32) return fast::launch_w<32>(kind, a, s, grid_out);
+    if (a.w <= 64) return fast::launch_w<64>(kind, a, s, grid_out);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {
+    if (nhub == 0) return cudaSuccess;
+    if (a.w <= 32) return fast::launch_hub_w<32>(sparse, a, hubs, nhub, s);
+    if (a.w <= 64) return fast::launch_hub_w<64>(sparse, a, hubs, nhub, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace gsrk

@@ -299,7 +299,7 @@ cudaError_t init_tile_w128();
 
 cudaError_t init_kernel_attributes() {
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {init_tile_w32(), init_tile_w64(), init_tile_w128()})
+    for (cudaError_t r : {init_tile_w32(), init_tile_w64(), init_tile_w128(), init_fast_attributes()})
         if (r != cudaSuccess) e = r;
     return e;
 }

@@ -21,6 +21,7 @@ namespace gsrk {
 
 constexpr int kThreads = 256;
 constexpr int kTileRows = 128;
+constexpr int kAggSeg = 8;  // canonical aggregation segment (== oracle kAggSeg, tile::kSeg)
 
 __host__ __device__ inline int rec_kh(int k) { return (k + 15) & ~15; }
 __host__ __device__ inline int rec_bytes(int k) { return (rec_kh(k) + 4 * k + 15) & ~15; }
@@ -81,6 +82,36 @@ struct TileArgs {
     double* part = nullptr;                // [gridDim.x][w*w + w]
     int tc = 0;                            // 1: transform on tcgen05 (TF32), 0: FP32-strict FFMA
 };
+
+// Thread-per-row tcgen05 fast path (fast.cu) for the GSR-C step in TF32 mode.
+// kind: 0 FWD (out = R + h, GS(out) → gs_out), 1 INV (out = R − h, dW/db
+// partials), 2 BIN (dst_p[r, I_m[r]] += h[r, I_m[r]], h = (Âᵀ·x_in)·Wᵀ).
+struct FastArgs {
+    int n = 0, w = 0, ld = 0, k = 0;       // k: records of rec_in
+    Dir dir;
+    const std::uint8_t* rec_in = nullptr;  // FWD / INV aggregation input
+    const float* x_in = nullptr;           // BIN aggregation input (dense plane)
+    float* Zh = nullptr;                   // hub-row aggregates (n × ld), written by k_hub
+    const float* Wm = nullptr;
+    const float* bias = nullptr;
+    int gemm_t = 0;                        // 0: h = Z·W, 1: h = Z·Wᵀ
+    const float* R = nullptr;
+    float* out = nullptr;
+    std::uint8_t* gs_out = nullptr;
+    int k_gs = 0;
+    const float* G = nullptr;              // INV: dW += Zᵀ·G
+    double* part = nullptr;                // INV: [grid][w*w + w]
+    int want_db = 0;
+    const std::uint8_t* mrec = nullptr;    // BIN: mask records
+    int k_m = 0;
+    float* dst[kMaxDst] = {};
+    int ndst = 0;
+};
+
+bool fast_supported(int w, int k);
+cudaError_t init_fast_attributes();
+cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s);
 
 // GS top-k of (sum of) planes: u = p0 + p1 + ... (left to right), records out.
 struct GsArgs {

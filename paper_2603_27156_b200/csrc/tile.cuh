@@ -194,6 +194,15 @@ struct AggMeta {
                                     hrow(meta + 2 * (TR + 1) + TR) {}
 };
 
+// Round to TF32 (10-bit mantissa, nearest, ties away): the operand the UMMA
+// kind::tf32 path consumes, made explicit so the oracle can mirror it
+// (oracle/gsr_oracle.hpp tf32_rna).
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 __device__ __forceinline__ uint4 ld4u(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
 struct SparseRec {  // one CBSR record with k ≤ 16: 16 index bytes + up to 16 values
@@ -441,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
             const int r = i / W, c = i % W;  // W[r][c], r = contraction index
             float v = 0.f;
             if (r < a.w && c < a.w) v = (a.gemm == GEMM_W) ? a.Wm[r * a.w + c] : a.Wm[c * a.w + r];
-            if constexpr (TC) Ws[boff<W>(c, r)] = v;  // Bᵀ[n = c][k = r]
+            if constexpr (TC) Ws[boff<W>(c, r)] = tf32_rna(v);  // Bᵀ[n = c][k = r]
             else Ws[i] = v;
         }
     }
@@ -509,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
                         const float f = rfs[r];
                         v.x = __fmul_rn(f, v.x); v.y = __fmul_rn(f, v.y); v.z = __fmul_rn(f, v.z); v.w = __fmul_rn(f, v.w);
                     }
+                    if (do_gemm) { v.x = tf32_rna(v.x); v.y = tf32_rna(v.y); v.z = tf32_rna(v.z); v.w = tf32_rna(v.w); }
                     *reinterpret_cast<float4*>(Zs + zoff(r, c)) = v;
                 }
                 fence_proxy_async();
@@ -664,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
                     for (int j = 0; j < 4; ++j) t[i][j] = 0.f;
                 for (int r = 0; r < TR; ++r) {
                     const float* gr = Et + r * ZLD + dn0;
-                    const float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3];
+                    float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3];
+                    if (TC && do_gemm) { g0 = tf32_rna(g0); g1 = tf32_rna(g1); g2 = tf32_rna(g2); g3 = tf32_rna(g3); }  // dW operands as the tensor core sees them
                     const float rf = (!TC && kScale) ? rfs[r] : 1.f;
 #pragma unroll
                     for (int i = 0; i < C::DMB; ++i) {

@@ -1,0 +1,137 @@
+"""Thread-per-row tcgen05 fast path (csrc/fast.cu) ↔ oracle in TF32 mode.
+
+The GSR-C step in TF32 mode runs k_fast FWD / INV / BIN plus the k_hub
+pre-pass for rows longer than one aggregation segment. The oracle in TF32 mode
+(oracle.set_tf32) rounds the same operands the kernels round (cvt.rna), so the
+two differ only by the tensor core's accumulation order; bounds as stated in
+tests/test_gpu_parity.py (TF32_ROW_RTOL per row for ≥ 99.5% of rows, masks
+≥ 99.5% identical, TF32_GRAD_RTOL on one layer's parameter gradients,
+TF32_STEP_RTOL on a multi-layer step's loss and gradients).
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import block_max_rel
+
+pytestmark = pytest.mark.gpu
+
+TF32_ROW_RTOL = 1e-4
+TF32_GRAD_RTOL = 1e-3   # one layer
+TF32_STEP_RTOL = 5e-3   # a multi-layer step: flipped near-tie masks compound across layers
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2603_27156_b200 import Context
+    return Context(0)
+
+
+@pytest.fixture
+def oracle_tf32(oracle):
+    oracle.set_tf32(True)
+    yield oracle
+    oracle.set_tf32(False)
+
+
+def _net(ctx, oracle, n, L, D, C, k, norm=1, hubs=(10, 60), hub_fraction=0.01, seed=0, use_bias=False, isolated=0):
+    from paper_2603_27156_b200 import GEMM_TF32, MODE_GSRC, model, synth
+    cfg = synth.SynthConfig(n=n, base_degree=2, hub_fraction=hub_fraction, hub_degree_range=hubs, seed=seed)
+    g, nd = synth.generate_synthetic(cfg)
+    if isolated:
+        rows = np.repeat(np.arange(n), np.diff(g.row_ptr))
+        keep = (rows >= isolated) & (g.col_idx >= isolated)
+        g = synth.from_edge_list(n, rows[keep], g.col_idx[keep])
+    ctx.graph_upload(g.row_ptr, g.col_idx, norm=norm)
+    og = oracle.Graph(g.row_ptr, g.col_idx, norm=norm)
+    ctx.model_init(MODE_GSRC, L, D, C, k, 8, use_bias=use_bias, gemm=GEMM_TF32)
+    net = oracle.Net(og, MODE_GSRC, L, D, C, k, 8, use_bias=use_bias, dtype=np.float32)
+    p = model.init_params(MODE_GSRC, L, D, C, 8, seed=seed + 1)
+    if use_bias:
+        lay = model.param_layout(MODE_GSRC, L, D, C, 8)
+        rng = np.random.default_rng(seed + 7)
+        for _, o, w in lay["blocks"]:
+            p[o + w * w:o + w * w + w] = rng.uniform(-0.05, 0.05, w)
+    ctx.set_params(p)
+    net.set_params(p)
+    ctx.data_upload(nd.features, nd.labels, nd.train_mask)
+    return g, nd, net, model.param_layout(MODE_GSRC, L, D, C, 8)
+
+
+def _rows_close(a, b):
+    err = np.abs(a - b).max(1) / max(np.abs(b).max(), 1e-30)
+    return (err <= TF32_ROW_RTOL).mean(), err
+
+
+@pytest.mark.parametrize("C,D,k,norm,bias", [(4, 256, 16, 1, False), (4, 128, 8, 1, True), (2, 64, 8, 2, False), (4, 256, 16, 0, False),
+                                             (8, 256, 8, 1, False), (2, 256, 16, 1, True)])
+def test_fast_layer_forward_backward(ctx, oracle_tf32, C, D, k, norm, bias):
+    """One GSR-C layer: forward (FWD), then backward (GS recompute, INV with dW,
+    BIN) from a random upstream gradient."""
+    oracle = oracle_tf32
+    n = 4000
+    _, _, net, lay = _net(ctx, oracle, n, 2, D, C, k, norm=norm, use_bias=bias)
+    rng = np.random.default_rng(D + C)
+    x = rng.normal(size=(n, D)).astype(np.float32)
+    ctx.set_activation(x)
+    ctx.layer_forward(0)
+    y = ctx.activation()
+    ry = net.layer_forward(0, x)
+    frac, err = _rows_close(y, ry)
+    assert frac >= 0.995, np.sort(err)[-10:]
+    gm = rng.normal(size=(n, D)).astype(np.float32)
+    ctx.set_activation(ry)
+    ctx.set_gradient(gm)
+    ctx.zero_grads()
+    net.zero_grads()
+    ctx.layer_backward(0)
+    rx, rg = net.layer_backward(0, ry, gm)
+    frac, err = _rows_close(ctx.activation(), rx)
+    assert frac >= 0.995, np.sort(err)[-10:]
+    frac, err = _rows_close(ctx.gradient(), rg)
+    assert frac >= 0.995, np.sort(err)[-10:]
+    gerr = block_max_rel(ctx.grads(), net.grads(), lay)
+    assert gerr <= TF32_GRAD_RTOL, gerr
+
+
+@pytest.mark.parametrize("C,D,k,hubs,iso", [(4, 256, 16, (10, 60), 0), (4, 256, 16, (900, 2500), 0), (2, 64, 8, (300, 700), 37)])
+def test_fast_train_step(ctx, oracle_tf32, C, D, k, hubs, iso):
+    """Whole step (encoder, L GSR-C layers, head, masked MSE, backward with
+    inverse recomputation): hub rows spanning several k_hub rounds (> 1024
+    edges), isolated rows, and one Adam step."""
+    oracle = oracle_tf32
+    n, L = 6000, 3
+    _, nd, net, lay = _net(ctx, oracle, n, L, D, C, k, hubs=hubs, hub_fraction=0.003, isolated=iso)
+    yhat = ctx.forward()
+    ryhat, _ = net.forward(nd.features)
+    # a near-tie GS mask flipped by the tensor core's accumulation order moves a
+    # handful of predictions: bound the bulk, not the max
+    close = np.abs(yhat - ryhat) <= TF32_ROW_RTOL * np.abs(ryhat).max()
+    assert close.mean() >= 0.995, np.sort(np.abs(yhat - ryhat))[-10:]
+    loss = ctx.forward_backward()
+    rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
+    assert abs(loss - rloss) <= TF32_STEP_RTOL * abs(rloss)
+    gerr = block_max_rel(ctx.grads(), rgrads, lay)
+    assert gerr <= TF32_STEP_RTOL, gerr
+    p0 = ctx.params()
+    ctx.optimizer_step(lr=1e-3)
+    assert np.isfinite(ctx.params()).all() and not np.array_equal(ctx.params(), p0)
+
+
+def test_fast_reversibility_roundtrip(ctx, oracle):
+    """forward then inverse on the device restores the layer input to ~1 ulp of
+    the output scale (size-independent property; the inverse recomputes the
+    same GS masks from the same bits)."""
+    from paper_2603_27156_b200 import GEMM_TF32, MODE_GSRC, model, synth
+    n, D, C, k = 20000, 256, 4, 16
+    g = synth.generate_graph(synth.SynthConfig(n=n, seed=3))
+    ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
+    ctx.model_init(MODE_GSRC, 3, D, C, k, 8, gemm=GEMM_TF32)
+    ctx.set_params(model.init_params(MODE_GSRC, 3, D, C, 8, seed=5, block_scale=0.3))
+    x = np.random.default_rng(0).normal(size=(n, D)).astype(np.float32)
+    ctx.set_activation(x)
+    for l in range(3):
+        ctx.layer_forward(l)
+    y = ctx.activation()
+    for l in reversed(range(3)):
+        ctx.layer_inverse(l)
+    assert np.abs(ctx.activation() - x).max() <= 1e-5 * np.abs(y).max()

@@ -254,21 +254,29 @@ def test_mem_peak_independent_of_depth(ctx, oracle):
     assert arena[(0, 64)] > arena[(0, 16)] > arena[(0, 4)]
 
 
-# ---- TF32 tensor-core transform (tcgen05) ------------------------------------
-# Stated looser bounds (north_star: "stated looser bounds for TF32/BF16"): the
-# transform's inputs are rounded to TF32 (10-bit mantissa) inside the tensor
-# core, so a row's output agrees with the FP32 oracle to ~1e-3 of its scale —
-# unless that perturbation flips a near-tie in a downstream GS top-k mask,
-# which swaps a selected column for that row. Bounds: ≥ 99% of rows within
-# 5e-3 of scale per layer, ≥ 99% of GS masks identical, and 2e-2 on
-# losses/gradients of a short network. (Exact-TF32 inputs reproduce the
-# oracle bit-for-bit: test_tf32_exact_inputs.)
-TF32_LAYER_RTOL = 5e-3
+# TF32 mode: the kernel rounds both transform operands to TF32 (cvt.rna) and
+# the tcgen05 core sums w exact products; the oracle in TF32 mode
+# (oracle.set_tf32) applies the same rounding, so the two differ only by the
+# accumulation order inside the tensor core (~1e-7 of a row's scale). A
+# difference that size can still flip a near-tie in a downstream GS top-k
+# mask, which swaps one selected column of that row. Stated TF32 bounds:
+# ≥ 99.5% of rows within 1e-4 of scale and ≥ 99.5% of GS masks identical per
+# layer; 1e-3 on losses / parameter gradients of a short network.
+TF32_ROW_RTOL = 1e-4
+TF32_GRAD_RTOL = 1e-3
+
+
+@pytest.fixture
+def oracle_tf32(oracle):
+    oracle.set_tf32(True)
+    yield oracle
+    oracle.set_tf32(False)
 
 
 @pytest.mark.parametrize("C,D,k", [(2, 64, 8), (4, 256, 16), (4, 128, 8)])
-def test_tf32_layer_forward_inverse(ctx, oracle, C, D, k):
+def test_tf32_layer_forward_inverse(ctx, oracle_tf32, C, D, k):
     from paper_2603_27156_b200 import GEMM_TF32
+    oracle = oracle_tf32
     n = 5000
     _, _, net, lay = _setup_net(ctx, oracle, 1, n, 2, D, C, k)
     ctx.model_init(1, 2, D, C, k, 8, use_bias=True, gemm=GEMM_TF32)
@@ -280,17 +288,20 @@ def test_tf32_layer_forward_inverse(ctx, oracle, C, D, k):
     y = ctx.activation()
     ry = net.layer_forward(0, x)
     row_err = np.abs(y - ry).max(1) / np.abs(ry).max()
-    assert (row_err <= TF32_LAYER_RTOL).mean() >= 0.99, np.sort(row_err)[-20:]
+    print("tf32 layer row err: median", np.median(row_err), "p99.5", np.quantile(row_err, 0.995), "max", row_err.max())
+    assert (row_err <= TF32_ROW_RTOL).mean() >= 0.995, np.sort(row_err)[-20:]
     w = D // C
     _, gi = oracle.gs_topk(y[:, :w], k)
     _, ri = oracle.gs_topk(ry[:, :w], k)
-    assert (gi == ri).all(1).mean() >= 0.99
+    assert (gi == ri).all(1).mean() >= 0.995
     ctx.layer_inverse(0)
-    assert np.abs(ctx.activation() - x).max() <= 1e-3 * np.abs(x).max()
+    # the inverse recomputes the forward's masks from the same bits: x = (x + h) - h to 1 ulp of y
+    assert np.abs(ctx.activation() - x).max() <= 1e-6 * np.abs(y).max()
 
 
-def test_tf32_train_step(ctx, oracle):
+def test_tf32_train_step(ctx, oracle_tf32):
     from paper_2603_27156_b200 import GEMM_TF32
+    oracle = oracle_tf32
     n, L, D, C, k = 4000, 4, 128, 4, 8
     _, nd, net, lay = _setup_net(ctx, oracle, 1, n, L, D, C, k)
     p = net.params()
@@ -299,8 +310,10 @@ def test_tf32_train_step(ctx, oracle):
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
     loss = ctx.forward_backward()
     rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
-    assert abs(loss - rloss) <= 2e-2 * abs(rloss)
-    assert block_max_rel(ctx.grads(), rgrads, lay) <= 2e-2
+    gerr = block_max_rel(ctx.grads(), rgrads, lay)
+    print("tf32 step: loss rel", abs(loss - rloss) / abs(rloss), "grad block rel", gerr)
+    assert abs(loss - rloss) <= TF32_GRAD_RTOL * abs(rloss)
+    assert gerr <= TF32_GRAD_RTOL
 
 
 def test_tf32_exact_inputs(ctx, oracle):

@@ -134,3 +134,21 @@ def test_gs_topk_k_out_of_range(oracle):
     with pytest.raises(oracle.OracleError) as e:
         oracle.gs_topk(np.zeros((2, 3)), 4)
     assert e.value.code == 1
+
+
+def test_oracle_tf32_rounding_rna(oracle):
+    """TF32 transform mode rounds operands to nearest, ties away (cvt.rna.tf32.f32)."""
+    rp, ci = np.arange(2), np.arange(1)
+    g = oracle.Graph(rp, ci, norm=0)
+    W = np.ones((1, 1), np.float32)
+    cases = [(1 + 2.0 ** -11, 1 + 2.0 ** -10), (1 + 2.0 ** -12, 1.0), (-(1 + 2.0 ** -11), -(1 + 2.0 ** -10)),
+             (1 + 3 * 2.0 ** -12, 1 + 2.0 ** -10)]
+    try:
+        oracle.set_tf32(True)
+        for x, want in cases:
+            out = oracle.block_fwd(g, np.array([[x]], np.float32), np.zeros((1, 1), np.int32), W, width=1)
+            assert out[0, 0] == np.float32(want), (x, out[0, 0], want)
+    finally:
+        oracle.set_tf32(False)
+    out = oracle.block_fwd(g, np.array([[1 + 2.0 ** -11]], np.float32), np.zeros((1, 1), np.int32), W, width=1)
+    assert out[0, 0] == np.float32(1 + 2.0 ** -11)
