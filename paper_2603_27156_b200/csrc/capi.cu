@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -242,7 +243,8 @@ struct gsrc_ctx {
     }
 
     // ---- thread-per-row tcgen05 fast path (fast.cu): GSR-C in TF32 mode ------
-    bool fast() const { return cfg.mode == GSRC_MODE_GSRC && cfg.gemm == GSRC_GEMM_TF32 && fast_supported(w, k); }
+    bool no_fast = std::getenv("GSRC_NO_FAST") != nullptr;  // A/B switch: generic k_tile for every block
+    bool fast() const { return !no_fast && cfg.mode == GSRC_MODE_GSRC && cfg.gemm == GSRC_GEMM_TF32 && fast_supported(w, k); }
     FastArgs fast_base(bool transpose) const {
         FastArgs f;
         f.n = static_cast<int>(n);

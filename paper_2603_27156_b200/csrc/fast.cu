@@ -55,10 +55,10 @@ __device__ __forceinline__ int zo(int r, int m) { return (m >> 5) * (TR * 32) + 
 __device__ __forceinline__ int zb(int r, int m) { return (m >> 5) * (TR * 32) + r * 32 + ((((m >> 3) & 3) ^ (r & 3)) << 3) + (m & 7); }
 
 // Shared memory (floats; every operand region 1 KB aligned):
-//   FWD: Ws | Zs | St      BIN: Ws | Zs      INV: Ws | Zs | Z2 | Gs
+//   FWD / BIN: Ws | Zs      INV: Ws | Zs | Z2 | Gs
 // Zs is the UMMA A operand; once the MMA has completed it holds the tile's
-// output rows (FWD: for the GS top-k; BIN: h for the masked scatter). St:
-// per-thread CBSR record staging (96 B). Z2 = Z and Gs = G in BASE32B
+// output rows (FWD: for the GS top-k; BIN: h for the masked scatter). Z2 = Z
+// and Gs = G in BASE32B
 // MN-major for dW. The residual row is read straight from global into
 // registers while the MMAs run.
 template <int W>
@@ -69,8 +69,7 @@ struct Plan {
     // stride from Z2); rows m ≥ W read past Z2 into Gs and land in TMEM lanes
     // that are never read, so Z2 + 4 atoms must stay inside the allocation.
     static constexpr int inv_tail = 2 * tile > 4 * TR * 32 ? 2 * tile : 4 * TR * 32;
-    static constexpr int stage = TR * 24;
-    static constexpr int floats(int kind) { return kind == INV ? ws + tile + inv_tail : (kind == FWD ? ws + tile + stage : ws + tile); }
+    static constexpr int floats(int kind) { return kind == INV ? ws + tile + inv_tail : ws + tile; }
     static constexpr size_t bytes(int kind) { return static_cast<size_t>(floats(kind) + 64) * sizeof(float); }
 };
 
@@ -121,46 +120,61 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
 
 // ---- sparse row aggregation (regular rows, deg ≤ kSeg) ----------------------
 // z[m] += sc · v over the row's edges in CSR order, the k (index, value)
-// pairs of each record in slot order — the oracle's spmm_sparse_row order.
-template <int W>
+// pairs of each record in slot order — the oracle's spmm_sparse_row order
+// (sc = 1 for unit edges: the multiply is exact). KS = k at compile time
+// (8 or 16), or 0 for any k ≤ 16 with predicated slots. The edge loop is not
+// unrolled (one record in flight ahead): the kernel's code must stay small
+// enough for the instruction cache.
+template <int W, int KS>
 __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
-    const int k = a.k;
+    const int k = KS ? KS : a.k;
     const int RB = rec_bytes(k), nv4 = (k + 3) >> 2;
     const bool unit = a.dir.unit_edge != 0;
-    int cs[kSegF];
+    int c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0;
+    const int c0 = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
+    if (ne > 1) c1 = __ldg(a.dir.idx + e0 + 1);
+    if (ne > 2) c2 = __ldg(a.dir.idx + e0 + 2);
+    if (ne > 3) c3 = __ldg(a.dir.idx + e0 + 3);
+    if (ne > 4) c4 = __ldg(a.dir.idx + e0 + 4);
+    if (ne > 5) c5 = __ldg(a.dir.idx + e0 + 5);
+    if (ne > 6) c6 = __ldg(a.dir.idx + e0 + 6);
+    if (ne > 7) c7 = __ldg(a.dir.idx + e0 + 7);
+    if (ne > 2) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
+    if (ne > 3) prefetch_l2(a.rec_in + static_cast<size_t>(c3) * RB);
+    const int rbase = r * 32;
+    const uint32_t rxx = static_cast<uint32_t>((r & 7) << 2) * 0x01010101u;
+    int cur_c = c0;
+    tile::SparseRec cur;
+    if (ne > 0) tile::load_rec16(cur, a.rec_in + static_cast<size_t>(c0) * RB, nv4);
+#pragma unroll 1
+    for (int u = 0; u < ne; ++u) {
+        const int nc = c1;  // shift register of the remaining neighbour ids
+        c1 = c2; c2 = c3; c3 = c4; c4 = c5; c5 = c6; c6 = c7;
+        tile::SparseRec nxt = cur;
+        if (u + 1 < ne) tile::load_rec16(nxt, a.rec_in + static_cast<size_t>(nc) * RB, nv4);
+        if (u + 3 < ne) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
+        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cur_c);
+        const uint32_t iw[4] = {cur.idx.x, cur.idx.y, cur.idx.z, cur.idx.w};
+        const float vv[16] = {cur.v[0].x, cur.v[0].y, cur.v[0].z, cur.v[0].w, cur.v[1].x, cur.v[1].y, cur.v[1].z, cur.v[1].w,
+                              cur.v[2].x, cur.v[2].y, cur.v[2].z, cur.v[2].w, cur.v[3].x, cur.v[3].y, cur.v[3].z, cur.v[3].w};
+        // a record's k indices are distinct: load all k accumulators, add,
+        // store (no read-after-write chain inside a record). Offsets are
+        // 32-bit shared-window indices; one LOP XOR-swizzles four index bytes
+        // (rx < 32 leaves bit 5, the 32-column region, intact).
+        constexpr int NJ = KS ? KS : 16;
+        int off[NJ];
+        float old[NJ];
 #pragma unroll
-    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + e0 + u) : 0;
-    float sc[kSegF];
-#pragma unroll
-    for (int u = 0; u < kSegF; ++u) sc[u] = (!unit && u < ne) ? __ldg(a.dir.edge_f + cs[u]) : 1.f;
-    const int rbase = r * 32, rx = (r & 7) << 2;
-#pragma unroll
-    for (int u = 1; u < kSegF; ++u)  // later records toward L2 while the first ones load
-        if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
-    tile::SparseRec buf[2];
-    if (ne > 0) tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
-#pragma unroll
-    for (int u = 0; u < kSegF; ++u) {
-        if (u < ne) {
-            if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
-            const tile::SparseRec& rc = buf[u & 1];
-            const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
-            const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
-                                  rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
-            // a record's k indices are distinct: load all k accumulators, add,
-            // store (no read-after-write chain inside a record)
-            float* zp[16];
-            float old[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int m = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                zp[j] = Zs + rbase + ((m ^ rx) & 31) + (m >> 5) * (TR * 32);
-                if (j < k) old[j] = *zp[j];
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (j < k) *zp[j] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc[u], vv[j]));
+        for (int j = 0; j < NJ; ++j) {
+            const int xb = static_cast<int>(__byte_perm(iw[j >> 2] ^ rxx, 0u, 0x4440u | static_cast<uint32_t>(j & 3)));  // m ^ rx, m < 64
+            off[j] = rbase + xb + (xb & 32) * (TR - 1);
+            if (KS || j < k) old[j] = Zs[off[j]];
         }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (KS || j < k) Zs[off[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
+        cur = nxt;
+        cur_c = nc;
     }
 }
 
@@ -168,47 +182,53 @@ __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, int e0, int ne
 template <int W>
 __device__ __forceinline__ void agg_dense_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
     const bool unit = a.dir.unit_edge != 0;
-    int cs[kSegF];
+    int c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0;
+    int c0 = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
+    if (ne > 1) c1 = __ldg(a.dir.idx + e0 + 1);
+    if (ne > 2) c2 = __ldg(a.dir.idx + e0 + 2);
+    if (ne > 3) c3 = __ldg(a.dir.idx + e0 + 3);
+    if (ne > 4) c4 = __ldg(a.dir.idx + e0 + 4);
+    if (ne > 5) c5 = __ldg(a.dir.idx + e0 + 5);
+    if (ne > 6) c6 = __ldg(a.dir.idx + e0 + 6);
+    if (ne > 7) c7 = __ldg(a.dir.idx + e0 + 7);
+    // every neighbour row toward L2 first: the per-edge row loads below then
+    // pay L2 latency, not DRAM latency
+    {
+        const int cc[kSegF] = {c0, c1, c2, c3, c4, c5, c6, c7};
 #pragma unroll
-    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + e0 + u) : 0;
-    float sc[kSegF];
-#pragma unroll
-    for (int u = 0; u < kSegF; ++u) sc[u] = (!unit && u < ne) ? __ldg(a.dir.edge_f + cs[u]) : 1.f;
-    constexpr int CH = 8;  // columns per pass: ne × 2 float4 loads in flight
-#pragma unroll 1
-    for (int c0 = 0; c0 < W; c0 += CH) {
-        float4 v[kSegF][CH / 4];
-#pragma unroll
-        for (int u = 0; u < kSegF; ++u)
-#pragma unroll
-            for (int q = 0; q < CH / 4; ++q)
-                v[u][q] = (u < ne && c0 + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(cs[u]) * a.ld + c0 + 4 * q)
-                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        float acc[CH];
-#pragma unroll
-        for (int q = 0; q < CH; ++q) acc[q] = 0.f;
-#pragma unroll
-        for (int u = 0; u < kSegF; ++u) {
-            if (u < ne) {
-#pragma unroll
-                for (int q = 0; q < CH / 4; ++q) {
-                    const float x[4] = {v[u][q].x, v[u][q].y, v[u][q].z, v[u][q].w};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) acc[4 * q + t] = __fadd_rn(acc[4 * q + t], unit ? x[t] : __fmul_rn(sc[u], x[t]));
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < CH / 4; ++q)
-            *reinterpret_cast<float4*>(Zs + zo(r, c0 + 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        for (int u = 1; u < kSegF; ++u)
+            if (u < ne) prefetch_l2_bulk(a.x_in + static_cast<size_t>(cc[u]) * a.ld, a.ld * 4);
     }
+    float acc[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) acc[q] = 0.f;
+#pragma unroll 1
+    for (int u = 0; u < ne; ++u) {
+        const int c = c0;
+        c0 = c1; c1 = c2; c2 = c3; c3 = c4; c4 = c5; c5 = c6; c6 = c7;
+        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
+        const float* src = a.x_in + static_cast<size_t>(c) * a.ld;
+        float4 x[W / 4];
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) x[q] = 4 * q < a.ld ? dev::ld4(src + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sc, x[q].x));
+            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sc, x[q].y));
+            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sc, x[q].z));
+            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sc, x[q].w));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q)
+        *reinterpret_cast<float4*>(Zs + zo(r, 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
 }
 
 // GS top-k of a row held in a swizzled smem tile → CBSR record.
 // Same selection as dev::gs_select_row: k-th largest magnitude key T via a
 // bitonic top-G tree, then columns ascending, ties at T lowest column first.
 template <int W, int G>
-__device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* stage, uint8_t* rec_out) {
+__device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
     uint32_t s[W];
 #pragma unroll
     for (int c = 0; c < W; c += 4) {
@@ -273,40 +293,64 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
 #pragma unroll
     for (int i = 0; i < G; ++i) gt += s[i] > T;
     int take = k - gt;
-    const int KH = rec_kh(k);
-    int slot = 0;
-    float* rv = reinterpret_cast<float*>(stage + KH);
+    // selection as a column bitmask: every key > T, plus the first `take` keys == T
+    constexpr int NWD = W / 32;
+    uint32_t gm[NWD], em[NWD];
+#pragma unroll
+    for (int q = 0; q < NWD; ++q) { gm[q] = 0u; em[q] = 0u; }
 #pragma unroll
     for (int c = 0; c < W; c += 4) {
         const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
         const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int col = c + t;
-            const uint32_t key = col < w ? dev::mag_key(vv[t]) : 0u;
-            const bool eq = key == T && col < w;
-            const bool pick = key > T || (eq && take > 0);
-            take -= (eq && take > 0) ? 1 : 0;
-            if (pick) {
-                stage[slot] = static_cast<uint8_t>(col);
-                rv[slot] = vv[t];
-                ++slot;
-            }
+        for (int q = 0; q < 4; ++q) {
+            const int col = c + q;
+            const uint32_t key = col < w ? dev::mag_key(vv[q]) : 0u;
+            gm[col >> 5] |= static_cast<uint32_t>(key > T) << (col & 31);
+            em[col >> 5] |= static_cast<uint32_t>(key == T) << (col & 31);
         }
     }
-    const int RB = rec_bytes(k);
-    for (int b = 0; b < RB; b += 16) *reinterpret_cast<uint4*>(rec_out + b) = *reinterpret_cast<const uint4*>(stage + b);
+#pragma unroll
+    for (int q = 0; q < NWD; ++q) {  // ties at T: lowest columns first
+        while (take > 0 && em[q]) {
+            gm[q] |= em[q] & (0u - em[q]);
+            em[q] &= em[q] - 1u;
+            --take;
+        }
+    }
+    // emit the k selected columns in ascending order with compile-time slots
+    // (k ≤ 16): index bytes and values assembled in registers, record written
+    // with 128-bit stores (layout: 16 index bytes, then k values, 16 B padded)
+    uint32_t iw[4] = {0u, 0u, 0u, 0u};
+    float rv[16];
+    uint32_t m0 = gm[0], m1 = NWD > 1 ? gm[NWD - 1] : 0u;
+#pragma unroll
+    for (int slot = 0; slot < 16; ++slot) {
+        rv[slot] = 0.f;
+        if (slot < k) {
+            int col;
+            if (m0) { col = __ffs(m0) - 1; m0 &= m0 - 1u; }
+            else { col = 32 + __ffs(m1) - 1; m1 &= m1 - 1u; }
+            iw[slot >> 2] |= static_cast<uint32_t>(col) << (8 * (slot & 3));
+            rv[slot] = Ts[zo(r, col)];
+        }
+    }
+    uint4* o = reinterpret_cast<uint4*>(rec_out);
+    o[0] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+    const int nv4 = (k + 3) >> 2;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (q < nv4) reinterpret_cast<float4*>(rec_out + 16)[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
 }
 
-template <int W, int KIND>
-__global__ void __launch_bounds__(TR, 1) k_fast(FastArgs a) {
+template <int W, int KIND, int KS>
+__global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k_fast(FastArgs a) {
     using Pl = Plan<W>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* base = reinterpret_cast<float*>(smem_raw);
     if ((smem_u32(base) & 1023u) != 0) __trap();  // UMMA SW128 atoms need 1 KB alignment
     float* Ws = base;
     float* Zs = Ws + Pl::ws;
-    float* St = Zs + Pl::tile;   // FWD
     float* Z2 = Zs + Pl::tile;   // INV
     float* Gs = Z2 + Pl::tile;   // INV
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(KIND));
@@ -368,7 +412,7 @@ __global__ void __launch_bounds__(TR, 1) k_fast(FastArgs a) {
                 } else if (KIND == BIN) {
                     agg_dense_row<W>(a, e0, ne, Zs, t);
                 } else {
-                    agg_sparse_row<W>(a, e0, ne, Zs, t);
+                    agg_sparse_row<W, KS>(a, e0, ne, Zs, t);
                 }
             }
             // Â row scale, then TF32 (the operand the tensor core consumes);
@@ -459,8 +503,7 @@ __global__ void __launch_bounds__(TR, 1) k_fast(FastArgs a) {
             }
         }
         if (KIND == FWD && a.gs_out && valid) {
-            uint8_t* stage = reinterpret_cast<uint8_t*>(St) + t * 96;
-            gs_row<W, 16>(Zs, t, a.w, a.k_gs, stage, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+            gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
         }
         if (KIND == BIN && valid) {
             const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
@@ -518,8 +561,8 @@ __global__ void __launch_bounds__(TR, 1) k_fast(FastArgs a) {
 // warp per segment for dense rows) into shared slots, then folded left to
 // right per column — the oracle's aggregation order for long rows.
 template <int W, bool SPARSE>
-__global__ void __launch_bounds__(128) k_hub(FastArgs a, const int* __restrict__ hubs) {
-    constexpr int NS = SPARSE ? (W >= 128 ? 64 : 128) : 16;  // segments per round (static smem ≤ 48 KB)
+__global__ void __launch_bounds__(SPARSE ? 64 : 128) k_hub(FastArgs a, const int* __restrict__ hubs) {
+    constexpr int NS = SPARSE ? 64 : 16;  // segments per round
     constexpr int PL = W + 4;  // 16 B aligned slot rows
     __shared__ __align__(16) float P[NS * PL];
     const int r = __ldg(hubs + blockIdx.x);
@@ -535,45 +578,65 @@ __global__ void __launch_bounds__(128) k_hub(FastArgs a, const int* __restrict__
                 float* pr = P + t * PL;
 #pragma unroll
                 for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int lo = e0 + (h0 + t) * kSegF, hi = min(e1, lo + kSegF);
+                const int lo = e0 + (h0 + t) * kSegF, ne = min(e1, lo + kSegF) - lo;
                 const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
-                for (int e = lo; e < hi; ++e) {
-                    const int c = __ldg(a.dir.idx + e);
-                    const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
-                    tile::SparseRec rc;
-                    tile::load_rec16(rc, a.rec_in + static_cast<size_t>(c) * RB, nv4);
-                    const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
-                    const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
-                                          rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
-                    float old[16];
-                    int mm[16];
+                int cs[kSegF];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        mm[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                        if (j < k) old[j] = pr[mm[j]];
+                for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
+#pragma unroll
+                for (int u = 1; u < kSegF; ++u)
+                    if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
+                tile::SparseRec buf[2];
+                tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
+#pragma unroll
+                for (int u = 0; u < kSegF; ++u) {
+                    if (u < ne) {
+                        if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
+                        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
+                        const tile::SparseRec& rc = buf[u & 1];
+                        const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
+                        const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
+                                              rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
+                        float old[16];
+                        int mm[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            mm[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                            if (j < k) old[j] = pr[mm[j]];
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < k) pr[mm[j]] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc, vv[j]));
                     }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < k) pr[mm[j]] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc, vv[j]));
                 }
             }
         } else {
             constexpr int CPL = W / 32 > 0 ? W / 32 : 1;
             for (int s = wid; s < nr; s += 4) {
-                const int lo = e0 + (h0 + s) * kSegF, hi = min(e1, lo + kSegF);
-                float acc[CPL];
+                const int lo = e0 + (h0 + s) * kSegF, ne = min(e1, lo + kSegF) - lo;
+                float x[kSegF][CPL];
 #pragma unroll
-                for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
-                for (int e = lo; e < hi; ++e) {
-                    const int c = __ldg(a.dir.idx + e);
-                    const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
+                for (int u = 0; u < kSegF; ++u) {  // all of the segment's row loads in flight
+                    const int c = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) {
                         const int col = lane + 32 * q;
-                        const float x = col < a.ld ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
-                        acc[q] = __fadd_rn(acc[q], unit ? x : __fmul_rn(sc, x));
+                        x[u][q] = (u < ne && col < a.ld) ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
+                    }
+                    if (!unit && u < ne) {
+                        const float sc = __ldg(a.dir.edge_f + c);
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) x[u][q] = __fmul_rn(sc, x[u][q]);
                     }
                 }
+                float acc[CPL];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+#pragma unroll
+                for (int u = 0; u < kSegF; ++u)
+                    if (u < ne)
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) acc[q] = __fadd_rn(acc[q], x[u][q]);
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) if (lane + 32 * q < W) P[s * PL + lane + 32 * q] = acc[q];
             }
@@ -596,7 +659,7 @@ __global__ void __launch_bounds__(128) k_hub(FastArgs a, const int* __restrict__
     if (t < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + t] = z;
 }
 
-template <int W, int KIND>
+template <int W, int KIND, int KS>
 int occupancy() {
     static int occ = 0;
     if (!occ) {
@@ -604,7 +667,7 @@ int occupancy() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, k_fast<W, KIND>);
+        cudaFuncGetAttributes(&fa, k_fast<W, KIND, KS>);
         const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(KIND) + 1024);  // + per-CTA reserved smem
         const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
         const int by_regs = 65536 / (regs * TR);
@@ -617,39 +680,52 @@ int occupancy() {
     return occ;
 }
 
-template <int W, int KIND>
+template <int W, int KIND, int KS>
 cudaError_t launch(const FastArgs& a, cudaStream_t s, int* grid_out) {
     const int tiles = (a.n + TR - 1) / TR;
-    const int cap = tile::sm_count_host() * occupancy<W, KIND>();
+    const int cap = tile::sm_count_host() * occupancy<W, KIND, KS>();
     const int grid = tiles < cap ? tiles : cap;
     if (grid_out) *grid_out = grid;
     if (grid == 0) return cudaSuccess;
-    k_fast<W, KIND><<<grid, TR, Plan<W>::bytes(KIND), s>>>(a);
+    k_fast<W, KIND, KS><<<grid, TR, Plan<W>::bytes(KIND), s>>>(a);
     return cudaGetLastError();
+}
+
+template <int W, int KIND, int KS>
+cudaError_t set_attr() {
+    return cudaFuncSetAttribute(k_fast<W, KIND, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(KIND)));
 }
 
 template <int W>
 cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {cudaFuncSetAttribute(k_fast<W, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(FWD))),
-                          cudaFuncSetAttribute(k_fast<W, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(INV))),
-                          cudaFuncSetAttribute(k_fast<W, BIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
+    for (cudaError_t r : {set_attr<W, FWD, 0>(), set_attr<W, FWD, 8>(), set_attr<W, FWD, 16>(), set_attr<W, INV, 0>(), set_attr<W, INV, 8>(),
+                          set_attr<W, INV, 16>(), set_attr<W, BIN, 0>()})
         if (r != cudaSuccess) e = r;
     return e;
+}
+
+// KS: record k as a compile-time constant when it is 8 or 16 (the configs'
+// values), else the predicated any-k variant.
+template <int W, int KIND>
+cudaError_t launch_k(const FastArgs& a, cudaStream_t s, int* g) {
+    if (a.k == 16) return launch<W, KIND, 16>(a, s, g);
+    if (a.k == 8) return launch<W, KIND, 8>(a, s, g);
+    return launch<W, KIND, 0>(a, s, g);
 }
 
 template <int W>
 cudaError_t launch_w(int kind, const FastArgs& a, cudaStream_t s, int* g) {
     switch (kind) {
-        case FWD: return launch<W, FWD>(a, s, g);
-        case INV: return launch<W, INV>(a, s, g);
-        default: return launch<W, BIN>(a, s, g);
+        case FWD: return launch_k<W, FWD>(a, s, g);
+        case INV: return launch_k<W, INV>(a, s, g);
+        default: return launch<W, BIN, 0>(a, s, g);
     }
 }
 
 template <int W>
 cudaError_t launch_hub_w(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {
-    if (sparse) k_hub<W, true><<<nhub, 128, 0, s>>>(a, hubs);
+    if (sparse) k_hub<W, true><<<nhub, 64, 0, s>>>(a, hubs);  // thread per segment, W ≤ 64 fold threads
     else k_hub<W, false><<<nhub, 128, 0, s>>>(a, hubs);
     return cudaGetLastError();
 }

