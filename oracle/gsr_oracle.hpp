@@ -303,20 +303,20 @@ void spmm_sparse(const Graph& g, bool transpose, int w, int k, const T* vals, co
 }
 
 // TF32 transform mode (the device's tcgen05 kind::tf32 path, GSRC_GEMM_TF32):
-// both operands of every block transform are rounded to TF32 (10-bit
-// mantissa, round-to-nearest ties-away, = PTX cvt.rna.tf32.f32, which the
-// kernel applies when it stages the UMMA operands). Products of two TF32
-// values are exact in FP32, so this oracle and the tensor core then differ
-// only by the accumulation order of w exact products.
+// both operands of every block transform are read as TF32, i.e. the low 13
+// mantissa bits truncated — what the tensor core does with fp32 operands
+// (measured on the B200: scratch/tf32_probe.cu, 128/128 truncation). Products
+// of two TF32 values are exact in FP32, so this oracle and the tensor core
+// then differ only by the accumulation order of w exact products.
 inline bool& tf32_transform() { static bool v = false; return v; }
-inline float tf32_rna(float x) {
+inline float tf32_op(float x) {
     std::uint32_t u;
     std::memcpy(&u, &x, 4);
-    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+    if ((u & 0x7f800000u) != 0x7f800000u) u &= 0xffffe000u;
     std::memcpy(&x, &u, 4);
     return x;
 }
-inline double tf32_rna(double x) { return static_cast<double>(tf32_rna(static_cast<float>(x))); }
+inline double tf32_op(double x) { return static_cast<double>(tf32_op(static_cast<float>(x))); }
 
 // One row of a dense transform: out[j] = fma-chain_m a[m]*B(m,j) (+0 start).
 // B(m,j) = b[m*ldb + j] (plain) or b[j*ldb + m] (transposed operand).
@@ -325,7 +325,7 @@ template <typename T>
 inline void gemm_row(const T* a, int K, int N, const T* b, index_t ldb, bool bt, T* out, bool rnd = false) {
     T acc[1024];
     for (int j = 0; j < N; ++j) acc[j] = T(0);
-    auto B = [&](T v) { return rnd ? static_cast<T>(tf32_rna(v)) : v; };
+    auto B = [&](T v) { return rnd ? static_cast<T>(tf32_op(v)) : v; };
     if (!bt) {
         for (int m = 0; m < K; ++m) {
             const T am = B(a[m]);
@@ -675,15 +675,21 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
             }
         });
         T* Gi = G + i * w;
-        if (f.use_weight) {
+        // dW_i = Zᵀ·G_i = (Â·S)ᵀ·G_i. FP32 (and REV) mode evaluates Zᵀ·G_i.
+        // TF32 GSR-C mode evaluates the same product as Sᵀ·(Âᵀ·G_i) from the
+        // tensor-core operands the device uses (its BIN kernel: S = the
+        // block's GS records, Âᵀ·G_i = the aggregation it already holds for the
+        // input gradient), both read as TF32 (tf32_op) — see below.
+        const bool tf32_sy = tf32_transform() && !rev && f.use_weight;
+        if (f.use_weight && !tf32_sy) {
             std::vector<double> acc;
-            // TF32 mode: dW = tf32(Z)ᵀ·tf32(G_i), the operands the device's dW tensor-core MMA consumes
             const bool rz = tf32_transform();
-            reduce_outer<T>(n, w, w, [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_rna(Z[r * w + j])) : Z[r * w + j]; },
-                            [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_rna(Gi[r * D + j])) : Gi[r * D + j]; }, acc);
+            reduce_outer<T>(n, w, w, [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_op(Z[r * w + j])) : Z[r * w + j]; },
+                            [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = rz ? static_cast<T>(tf32_op(Gi[r * D + j])) : Gi[r * D + j]; }, acc);
             T* dw = net.dW(l, i);
             for (int q = 0; q < w * w; ++q) dw[q] = static_cast<T>(static_cast<double>(dw[q]) + acc[q]);
         }
+        std::vector<T> Yb(tf32_sy ? static_cast<size_t>(n) * w : 0);
         if (f.use_bias) {
             std::vector<double> acc;
             colsum<T>(n, w, Gi, D, acc);
@@ -695,6 +701,7 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
             T yt[1024], t[1024];
             for (index_t r = b; r < e; ++r) {
                 spmm_row(bwd, r, w, Gi, D, yt);
+                if (tf32_sy) std::memcpy(Yb.data() + r * w, yt, sizeof(T) * w);
                 if (f.use_weight) gemm_row(yt, w, w, net.W(l, i), w, true, t, tf32_transform());
                 else for (int j = 0; j < w; ++j) t[j] = yt[j];
                 auto add_to = [&](T* dst) {
@@ -708,6 +715,17 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
                 else for (int j = 1; j < C; ++j) add_to(G + r * D + j * w);
             }
         });
+        if (tf32_sy) {
+            std::vector<double> acc;
+            reduce_outer<T>(n, w, w,
+                [&](index_t r, T* x) {
+                    for (int j = 0; j < w; ++j) x[j] = T(0);
+                    for (int j = 0; j < k; ++j) x[a.idx[r * k + j]] = static_cast<T>(tf32_op(a.vals[r * k + j]));
+                },
+                [&](index_t r, T* x) { for (int j = 0; j < w; ++j) x[j] = static_cast<T>(tf32_op(Yb[r * w + j])); }, acc);
+            T* dw = net.dW(l, i);
+            for (int q = 0; q < w * w; ++q) dw[q] = static_cast<T>(static_cast<double>(dw[q]) + acc[q]);
+        }
     }
 }
 

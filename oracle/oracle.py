@@ -65,8 +65,9 @@ def _sfx(dtype):
 
 
 def set_tf32(on):
-    """TF32 transform mode: round both operands of every block transform to TF32
-    (cvt.rna), as the device's tcgen05 kind::tf32 path stages them."""
+    """TF32 transform mode: both operands of every block transform (and of the
+    GSR-C dW product) read as TF32 by truncation, as the B200 tensor core reads
+    fp32 operands (measured: scratch/tf32_probe.cu)."""
     _chk(lib().gsro_set_tf32(int(bool(on))))
 
 

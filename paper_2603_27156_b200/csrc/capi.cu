@@ -144,6 +144,7 @@ struct gsrc_ctx {
     // activation arena
     Arena arena;
     float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr, *Zh = nullptr;
+    std::vector<CUtensorMap> xmaps;  // TMA maps of the X planes (fast path)
     uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
     std::vector<uint8_t*> c1, c2;
     std::vector<char> filled;
@@ -274,6 +275,7 @@ struct gsrc_ctx {
         f.bias = Bb(l, i);
         f.R = plane(X, i);
         f.out = plane(X, i);
+        f.tm_x = xmaps[static_cast<size_t>(i)];
         f.gs_out = gs_out;
         f.k_gs = k;
         run_fast(0, f);
@@ -281,8 +283,14 @@ struct gsrc_ctx {
     // Eq. 7 inverse of block i + dW/db, then the masked input gradient
     void fast_block_backward(int l, int i, const uint8_t* rec) {
         fast_inverse(l, i, rec);
-        reduce_block_grads(l, i);
         fast_input_grad(l, i, rec);
+        reduce_block_grads(l, i);  // dW = Sᵀ·(Âᵀ·G_i) partials from BIN
+        if (cfg.use_bias) {        // db = colsum(G_i)
+            CK(launch_colsum(plane(G, i), static_cast<int>(n), w, ld, part, &last_grid, stream));
+            ++launches;
+            CK(launch_reduce_parts(part, last_grid, w, w, grads + off_block(l, i) + static_cast<size_t>(w) * w, 1, stream));
+            ++launches;
+        }
     }
     void fast_inverse(int l, int i, const uint8_t* rec) {
         FastArgs f = fast_base(false);
@@ -292,9 +300,7 @@ struct gsrc_ctx {
         f.bias = Bb(l, i);
         f.R = plane(X, i);
         f.out = plane(X, i);
-        f.G = plane(G, i);
-        f.part = part;
-        f.want_db = cfg.use_bias;
+        f.tm_x = xmaps[static_cast<size_t>(i)];
         run_fast(1, f);
     }
     void fast_input_grad(int l, int i, const uint8_t* rec) {
@@ -305,6 +311,7 @@ struct gsrc_ctx {
         b.gemm_t = 1;
         b.mrec = rec;
         b.k_m = k;
+        b.part = part;
         if (i > 0) { b.dst[0] = plane(G, i - 1); b.ndst = 1; }
         else { for (int p = 1; p < C; ++p) b.dst[p - 1] = plane(G, p); b.ndst = C - 1; }
         run_fast(2, b);
@@ -540,6 +547,9 @@ struct gsrc_ctx {
         U = nullptr;
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
         Zh = fast() ? arena.lease<float>(pl) : nullptr;
+        xmaps.assign(static_cast<size_t>(C), CUtensorMap{});
+        if (fast())
+            for (int p = 0; p < C; ++p) CK(encode_plane_map(&xmaps[static_cast<size_t>(p)], plane(X, p), static_cast<int>(n), ld));
         c1.clear();
         c2.clear();
         if (alg12) {
@@ -1239,7 +1249,7 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         TileArgs ra = fa;
         ra.epi = EPI_SUB; ra.gs_out = nullptr; ra.G = ctx->plane(ctx->G, 1); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
         if (!fp) out[4] = time_it([&] { ctx->run_tile(ra); });
-        out[5] = csr + n * rb + 12 * n * w;
+        out[5] = csr + n * rb + ((ctx->fast() && ctx->cfg.use_weight) ? 8 : 12) * n * w;  // fast path: dW rides on BIN
         out[6] = L * C;
         out[7] = 4 * n * w * w;
         TileArgs ba = ctx->tile_base();

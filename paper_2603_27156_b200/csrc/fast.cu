@@ -8,9 +8,11 @@
 //   FWD  y'_i = x_i + (Â·scatter(V,I))·W_i + b_i, then GS_k(y'_i) → records
 //        (gsr_forward_block SPEC.md:253-261 + Eq. 6 add + gs_topk SPEC.md:67-76)
 //   INV  x_i = y'_i − (Â·scatter(V,I))·W_i − b_i   (Eq. 7)
-//        + dW_i += Zᵀ·G_i on the tensor core (db_i += colsum G_i)
-//   BIN  dst_p[r, I[r]] += ((Âᵀ·G_i)·W_iᵀ)[r, I[r]]  (exact GS-masked input
-//        gradient, SPEC.md:262-270 restated for Eq. 6-7)
+//   BIN  Y = Âᵀ·G_i;  dst_p[r, I[r]] += (Y·W_iᵀ)[r, I[r]]  (exact GS-masked
+//        input gradient, SPEC.md:262-270 restated for Eq. 6-7) and
+//        dW_i += Sᵀ·Y = (Â·S)ᵀ·G_i, S = scatter(V,I), on the tensor core — the
+//        parameter gradient rides on the aggregation BIN already does, so the
+//        inverse pass never reads G_i (db_i = colsum G_i: k_colsum, bias only)
 //
 // Design (one CTA = 128 threads = one 128-row tile at a time, persistent):
 //   * thread t owns tile row t end to end: it walks its CSR edges (≤ kSeg;
@@ -23,10 +25,13 @@
 //   * the residual / gradient row tiles are staged with cp.async (LDGSTS)
 //     into swizzled shared memory while the aggregation runs;
 //   * one elected thread issues tcgen05.mma kind::tf32 (M = 128, N = W) and,
-//     for INV, a second MN-major MMA accumulating dW = Zᵀ·G in TMEM across all
+//     for BIN, a second MN-major MMA accumulating dW = Sᵀ·Y in TMEM across all
 //     tiles of the CTA (per-CTA partials, reduced in fixed order afterwards).
 // Arithmetic per row is the oracle's (oracle/gsr_oracle.hpp, TF32 mode):
-// canonical segmented aggregation, row scale, cvt.rna TF32 operands.
+// canonical segmented aggregation, row scale; fp32 operands are handed to the
+// tensor core as they are, which reads them as TF32 by truncating the low 13
+// mantissa bits (measured on the device, scratch/tf32_probe.cu) — the oracle
+// truncates the same operands.
 #include "tile.cuh"
 
 namespace gsrk {
@@ -35,7 +40,6 @@ namespace fast {
 using tile::mbar_init;
 using tile::mbar_wait;
 using tile::smem_u32;
-using tile::tf32_rna;
 using tile::tmem_ld;
 
 constexpr int TR = 128;       // rows per tile == threads per CTA
@@ -55,21 +59,20 @@ __device__ __forceinline__ int zo(int r, int m) { return (m >> 5) * (TR * 32) + 
 __device__ __forceinline__ int zb(int r, int m) { return (m >> 5) * (TR * 32) + r * 32 + ((((m >> 3) & 3) ^ (r & 3)) << 3) + (m & 7); }
 
 // Shared memory (floats; every operand region 1 KB aligned):
-//   FWD / BIN: Ws | Zs      INV: Ws | Zs | Z2 | Gs
+//   FWD / INV: Ws | Zs      BIN: Ws | Zs | Y2
 // Zs is the UMMA A operand; once the MMA has completed it holds the tile's
-// output rows (FWD: for the GS top-k; BIN: h for the masked scatter). Z2 = Z
-// and Gs = G in BASE32B
-// MN-major for dW. The residual row is read straight from global into
-// registers while the MMAs run.
+// output rows (FWD: for the GS top-k; BIN: h for the masked scatter, then S
+// in BASE32B MN-major for dW). Y2 = Y in BASE32B MN-major for dW. The
+// residual row is read straight from global into registers while the MMA runs.
 template <int W>
 struct Plan {
     static constexpr int ws = W * W;
     static constexpr int tile = TR * W;
-    // the dW MMA runs with M = 128 (A = Zᵀ: four 32-column atoms at TR·128 B
-    // stride from Z2); rows m ≥ W read past Z2 into Gs and land in TMEM lanes
-    // that are never read, so Z2 + 4 atoms must stay inside the allocation.
-    static constexpr int inv_tail = 2 * tile > 4 * TR * 32 ? 2 * tile : 4 * TR * 32;
-    static constexpr int floats(int kind) { return kind == INV ? ws + tile + inv_tail : ws + tile; }
+    // the dW MMA runs with M = 128 (A = Sᵀ: four 32-column atoms at TR·128 B
+    // stride from Zs); rows m ≥ W read past Zs into Y2 and land in TMEM lanes
+    // that are never read, so Zs + 4 atoms must stay inside the allocation.
+    static constexpr int bin_tail = 2 * tile > 4 * TR * 32 ? 2 * tile : 4 * TR * 32;
+    static constexpr int floats(int kind) { return kind == BIN ? ws + bin_tail : ws + tile; }
     static constexpr size_t bytes(int kind) { return static_cast<size_t>(floats(kind) + 64) * sizeof(float); }
 };
 
@@ -80,6 +83,24 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// ---- TMA (cp.async.bulk.tensor) for the residual / output row tiles ----------
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int r0) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(m), "r"(c0), "r"(r0) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, void* dst, uint64_t* bar, int c0, int r0) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(r0), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int r0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(m), "r"(c0), "r"(r0), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -344,30 +365,29 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
 }
 
 template <int W, int KIND, int KS>
-__global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k_fast(FastArgs a) {
+__global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* base = reinterpret_cast<float*>(smem_raw);
     if ((smem_u32(base) & 1023u) != 0) __trap();  // UMMA SW128 atoms need 1 KB alignment
     float* Ws = base;
     float* Zs = Ws + Pl::ws;
-    float* Z2 = Zs + Pl::tile;   // INV
-    float* Gs = Z2 + Pl::tile;   // INV
+    float* Y2 = Zs + Pl::tile;   // BIN
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(KIND));
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int t = threadIdx.x, wid = t >> 5;
     const int n_tiles = (a.n + TR - 1) / TR;
-    constexpr uint32_t TCOLS = KIND == INV ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+    constexpr uint32_t TCOLS = KIND == BIN ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
 
-    // transform operand Bᵀ[n][m] (K-major SW128, region stride W·32), TF32-rounded
+    // transform operand Bᵀ[n][m] (K-major SW128, region stride W·32)
     for (int i = t; i < W * W; i += TR) {
         const int r = i / W, c = i % W;  // contraction index r, output column c
         float v = 0.f;
         if (r < a.w && c < a.w) v = a.gemm_t ? a.Wm[c * a.w + r] : a.Wm[r * a.w + c];
-        Ws[tile::boff<W>(c, r)] = tf32_rna(v);
+        Ws[tile::boff<W>(c, r)] = v;
     }
-    if (t == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
+    if (t == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1); }
     if (wid == 0) tile::tmem_alloc(tslot, TCOLS);
     tile::fence_proxy_async();
     tile::tc_fence_before();
@@ -375,25 +395,26 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
     tile::tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t tlane = static_cast<uint32_t>(32 * wid) << 16;
-    uint32_t ph0 = 0, ph1 = 0;
+    uint32_t ph0 = 0, ph1 = 0, ph2 = 0;
     bool dw_pending = false;
-    double dbsum = 0.0;
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR;
         const int row = row0 + t;
         const bool valid = row < a.n;
-        if (KIND == INV && dw_pending) {  // previous dW MMA still reads Zs / Gs
+        if (KIND == BIN && dw_pending) {  // previous dW MMA still reads Zs / Y2
             mbar_wait(&bar[1], ph1);
             ph1 ^= 1u;
             tile::tc_fence_after();
             dw_pending = false;
         }
         // stage the residual (FWD / INV) and gradient (INV) rows
-        if (KIND == INV) stage_tile<W, true>(Gs, a.G, row0, a.n, a.ld);
 
-        // residual row toward L2 now; it is loaded into registers while the MMA runs
-        if (KIND != BIN && valid && row0 + TR <= a.n) prefetch_l2_bulk(a.R + static_cast<size_t>(row) * a.ld, a.ld * 4);
+        // residual tile toward L2 now (TMA prefetch); it is TMA-loaded into Zs
+        // once the MMA has consumed the A operand
+        if (KIND != BIN && t == 0)
+#pragma unroll
+            for (int c = 0; c < W; c += 32) tma_prefetch_2d(&a.tm_x, c, row0);
         // ---- aggregation into this thread's row of the A operand
         {
             const int rbase = t * 32, rx = (t & 7) << 2;
@@ -415,34 +436,14 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
                     agg_sparse_row<W, KS>(a, e0, ne, Zs, t);
                 }
             }
-            // Â row scale, then TF32 (the operand the tensor core consumes);
-            // INV also keeps the row in the MN-major layout for dW
+            // Â row scale (BIN also keeps Y in the MN-major layout for dW)
 #pragma unroll
             for (int c = 0; c < W; c += 4) {
                 float4* p = reinterpret_cast<float4*>(Zs + zo(t, c));
                 float4 v = *p;
-                v.x = tf32_rna(__fmul_rn(rf, v.x)); v.y = tf32_rna(__fmul_rn(rf, v.y));
-                v.z = tf32_rna(__fmul_rn(rf, v.z)); v.w = tf32_rna(__fmul_rn(rf, v.w));
+                v.x = __fmul_rn(rf, v.x); v.y = __fmul_rn(rf, v.y); v.z = __fmul_rn(rf, v.z); v.w = __fmul_rn(rf, v.w);
                 *p = v;
-                if (KIND == INV) *reinterpret_cast<float4*>(Z2 + zb(t, c)) = v;
-            }
-        }
-        if (KIND != BIN) cp_async_wait_all();  // this thread's staged chunks
-        if (KIND == INV) {
-            __syncthreads();  // G rows staged by other threads
-            if (a.want_db && t < a.w) {  // db = colsum(G) in row order, unrounded
-                float s = 0.f;
-                for (int r = 0; r < TR; ++r) s = __fadd_rn(s, Gs[zb(r, t)]);
-                dbsum += static_cast<double>(s);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int c = 0; c < W; c += 4) {  // dW's B operand in TF32
-                float4* p = reinterpret_cast<float4*>(Gs + zb(t, c));
-                float4 v = *p;
-                if (!valid) v = make_float4(0.f, 0.f, 0.f, 0.f);
-                v.x = tf32_rna(v.x); v.y = tf32_rna(v.y); v.z = tf32_rna(v.z); v.w = tf32_rna(v.w);
-                *p = v;
+                if (KIND == BIN) *reinterpret_cast<float4*>(Y2 + zb(t, c)) = v;
             }
         }
         tile::fence_proxy_async();
@@ -455,27 +456,19 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
                 umma(tmem, desc_sw128(za + (kk >> 2) * (TR * 128) + (kk & 3) * 32, 16), desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16),
                      idesc<W>(0, 0), kk > 0 ? 1u : 0u);
             tile::umma_commit(&bar[0]);
-            if (KIND == INV) {
-                // dW[m][n] += Σ_r Z[r][m] G[r][n]: A = Zᵀ, B = G, both MN-major
-                // BASE32B (rows = K: 4-row groups at 512 B, 32-col atoms at TR·128 B)
-                const uint32_t z2 = smem_u32(Z2), ga = smem_u32(Gs);
-                const bool first = tile_i == static_cast<int>(blockIdx.x);
-#pragma unroll
-                for (int kk = 0; kk < TR / 8; ++kk)
-                    umma(tmem + W, desc_mn32(z2 + kk * 1024), desc_mn32(ga + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
-                tile::umma_commit(&bar[1]);
-            }
-        }
-        if (KIND == INV) dw_pending = true;
-        float4 Rg[KIND != BIN ? W / 4 : 1];
-        if (KIND != BIN) {  // residual row straight from global while the MMA runs
-#pragma unroll
-            for (int c = 0; c < W; c += 4)
-                Rg[c / 4] = (valid && c < a.ld) ? *reinterpret_cast<const float4*>(a.R + static_cast<size_t>(row) * a.ld + c) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         mbar_wait(&bar[0], ph0);
         ph0 ^= 1u;
         tile::tc_fence_after();
+        if (KIND != BIN) {  // the MMA has read Zs: bring the residual tile in (rows ≥ n read as 0)
+            if (t == 0) {
+                mbar_expect_tx(&bar[2], static_cast<uint32_t>(TR * W * 4));
+#pragma unroll
+                for (int c = 0; c < W; c += 32) tma_load_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), &bar[2], c, row0);
+            }
+            mbar_wait(&bar[2], ph2);
+            ph2 ^= 1u;
+        }
 
         // ---- epilogue: this thread's accumulator row (TMEM lane = tile row)
 #pragma unroll
@@ -494,17 +487,26 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
                 }
                 float4* rp = reinterpret_cast<float4*>(Zs + zo(t, c));
                 if (KIND != BIN) {
-                    const float4 R = Rg[c / 4];
+                    const float4 R = *rp;
                     if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
                     else { o[0] = __fsub_rn(R.x, o[0]); o[1] = __fsub_rn(R.y, o[1]); o[2] = __fsub_rn(R.z, o[2]); o[3] = __fsub_rn(R.w, o[3]); }
-                    if (valid && c < a.ld) *reinterpret_cast<float4*>(a.out + static_cast<size_t>(row) * a.ld + c) = make_float4(o[0], o[1], o[2], o[3]);
                 }
-                if (KIND != INV) *rp = make_float4(o[0], o[1], o[2], o[3]);  // row kept for GS / masked scatter
+                *rp = make_float4(o[0], o[1], o[2], o[3]);  // output row: TMA store source, GS input / masked-scatter h
+            }
+        }
+        if (KIND != BIN) {  // output tile back in place by TMA (rows ≥ n clipped)
+            tile::fence_proxy_async();
+            __syncthreads();
+            if (t == 0) {
+#pragma unroll
+                for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), c, row0);
+                tma_store_commit();
             }
         }
         if (KIND == FWD && a.gs_out && valid) {
             gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
         }
+        if (KIND != BIN && t == 0) tma_store_wait_read();  // Zs is rewritten by the next tile
         if (KIND == BIN && valid) {
             const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
             const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
@@ -526,10 +528,35 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
                 for (int j = 0; j < 16; ++j) if (j < a.k_m) d[col[j]] = __fadd_rn(o[j], v[j]);
             }
         }
+        if (KIND == BIN) {
+            // S = scatter(V, I) of this row (the block's sparse input) over its own
+            // h row, in the MN-major layout: dW += Sᵀ·Y (A = Sᵀ, B = Y2)
+#pragma unroll
+            for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Zs + zb(t, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) {
+                const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
+                const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
+                const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
+                const float* rv = reinterpret_cast<const float*>(rc + rec_kh(a.k_m));
+                for (int j = 0; j < a.k_m; ++j) Zs[zb(t, static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu))] = rv[j];
+            }
+            tile::fence_proxy_async();
+            __syncthreads();
+            if (t == 0) {
+                tile::tc_fence_after();
+                const uint32_t sa = smem_u32(Zs), ya = smem_u32(Y2);
+                const bool first = tile_i == static_cast<int>(blockIdx.x);
+#pragma unroll
+                for (int kk = 0; kk < TR / 8; ++kk)
+                    umma(tmem + W, desc_mn32(sa + kk * 1024), desc_mn32(ya + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
+                tile::umma_commit(&bar[1]);
+            }
+            dw_pending = true;
+        }
         tile::tc_fence_before();
         __syncthreads();
     }
-    if (KIND == INV) {
+    if (KIND == BIN) {
         if (dw_pending) {
             mbar_wait(&bar[1], ph1);
             tile::tc_fence_after();
@@ -549,7 +576,7 @@ __global__ void __launch_bounds__(TR, KIND == INV ? 2 : (KIND == FWD ? 4 : 3)) k
                     if (c0 + j < a.w) pp[m * a.w + c0 + j] = any ? static_cast<double>(v[j]) : 0.0;
             }
         }
-        if (t < a.w) pp[a.w * a.w + t] = a.want_db ? dbsum : 0.0;
+        if (t < a.w) pp[a.w * a.w + t] = 0.0;  // db: k_colsum (bias only)
     }
     tile::tc_fence_before();
     __syncthreads();
@@ -659,6 +686,21 @@ __global__ void __launch_bounds__(SPARSE ? 64 : 128) k_hub(FastArgs a, const int
     if (t < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + t] = z;
 }
 
+// db = colsum(G) (bias only): per-CTA partials over 128-row tiles in row
+// order (float within a tile, double across tiles), reduced in fixed order.
+__global__ void __launch_bounds__(128) k_colsum(const float* __restrict__ G, int n, int w, int ld, double* __restrict__ part) {
+    const int t = threadIdx.x;
+    double acc = 0.0;
+    for (int r0 = blockIdx.x * TR; r0 < n; r0 += gridDim.x * TR) {
+        float s = 0.f;
+        const int r1 = min(n, r0 + TR);
+        if (t < w)
+            for (int r = r0; r < r1; ++r) s = __fadd_rn(s, __ldg(G + static_cast<size_t>(r) * ld + t));
+        acc += static_cast<double>(s);
+    }
+    if (t < w) part[static_cast<size_t>(blockIdx.x) * w + t] = acc;
+}
+
 template <int W, int KIND, int KS>
 int occupancy() {
     static int occ = 0;
@@ -671,7 +713,7 @@ int occupancy() {
         const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(KIND) + 1024);  // + per-CTA reserved smem
         const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
         const int by_regs = 65536 / (regs * TR);
-        constexpr int tcols = KIND == INV ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+        constexpr int tcols = KIND == BIN ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
         occ = by_smem < by_regs ? by_smem : by_regs;
         if (occ > 512 / tcols) occ = 512 / tcols;
         if (occ > 8) occ = 8;
@@ -732,6 +774,26 @@ cudaError_t launch_hub_w(bool sparse, const FastArgs& a, const int* hubs, int nh
 
 }  // namespace fast
 
+cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        enc = reinterpret_cast<Encode>(fn);
+    }
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(n)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(fast::TR)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // W = 128 would need 256 KB of shared memory for INV: k_tile serves it.
 bool fast_supported(int w, int k) { return w >= 1 && w <= 64 && k >= 1 && k <= 16; }
 
@@ -750,6 +812,15 @@ cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_o
     if (a.w <= 32) return fast::launch_w<32>(kind, a, s, grid_out);
     if (a.w <= 64) return fast::launch_w<64>(kind, a, s, grid_out);
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, int* grid_out, cudaStream_t s) {
+    const int tiles = (n + fast::TR - 1) / fast::TR;
+    const int cap = tile::sm_count_host() * 8;
+    const int grid = tiles < cap ? (tiles > 0 ? tiles : 1) : cap;
+    if (grid_out) *grid_out = grid;
+    fast::k_colsum<<<grid, 128, 0, s>>>(G, n, w, ld, part);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {

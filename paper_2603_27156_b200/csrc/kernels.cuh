@@ -15,6 +15,7 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace gsrk {
@@ -84,8 +85,9 @@ struct TileArgs {
 };
 
 // Thread-per-row tcgen05 fast path (fast.cu) for the GSR-C step in TF32 mode.
-// kind: 0 FWD (out = R + h, GS(out) → gs_out), 1 INV (out = R − h, dW/db
-// partials), 2 BIN (dst_p[r, I_m[r]] += h[r, I_m[r]], h = (Âᵀ·x_in)·Wᵀ).
+// kind: 0 FWD (out = R + h, GS(out) → gs_out), 1 INV (out = R − h),
+// 2 BIN (dst_p[r, I_m[r]] += h[r, I_m[r]], h = (Âᵀ·x_in)·Wᵀ; dW partials
+// += scatter(mrec)ᵀ·(Âᵀ·x_in)).
 struct FastArgs {
     int n = 0, w = 0, ld = 0, k = 0;       // k: records of rec_in
     Dir dir;
@@ -96,22 +98,25 @@ struct FastArgs {
     const float* bias = nullptr;
     int gemm_t = 0;                        // 0: h = Z·W, 1: h = Z·Wᵀ
     const float* R = nullptr;
-    float* out = nullptr;
+    float* out = nullptr;                  // FWD / INV: out aliases R (in place), moved by TMA through tm_x
     std::uint8_t* gs_out = nullptr;
     int k_gs = 0;
-    const float* G = nullptr;              // INV: dW += Zᵀ·G
-    double* part = nullptr;                // INV: [grid][w*w + w]
-    int want_db = 0;
+    double* part = nullptr;                // BIN: dW partials [grid][w*w + w]
     const std::uint8_t* mrec = nullptr;    // BIN: mask records
     int k_m = 0;
     float* dst[kMaxDst] = {};
     int ndst = 0;
+    CUtensorMap tm_x;                      // FWD / INV: 2-D tiled map of the R/out plane (128 rows × 32 cols, SWIZZLE_128B)
 };
 
 bool fast_supported(int w, int k);
+// TMA map of an n × ld fp32 plane in 128-row × 32-column boxes, SWIZZLE_128B
+// (the boxes land in exactly the UMMA K-major SW128 tile layout of fast.cu).
+cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld);
 cudaError_t init_fast_attributes();
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s);
+cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, int* grid_out, cudaStream_t s);
 
 // GS top-k of (sum of) planes: u = p0 + p1 + ... (left to right), records out.
 struct GsArgs {

@@ -194,14 +194,10 @@ struct AggMeta {
                                     hrow(meta + 2 * (TR + 1) + TR) {}
 };
 
-// Round to TF32 (10-bit mantissa, nearest, ties away): the operand the UMMA
-// kind::tf32 path consumes, made explicit so the oracle can mirror it
-// (oracle/gsr_oracle.hpp tf32_rna).
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
+// An fp32 value as the UMMA kind::tf32 path reads it: low 13 mantissa bits
+// truncated (measured on the B200, scratch/tf32_probe.cu; oracle tf32_op).
+// Used where the CUDA cores must reproduce a tensor-core operand.
+__device__ __forceinline__ float tf32_op(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 __device__ __forceinline__ uint4 ld4u(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
@@ -450,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
             const int r = i / W, c = i % W;  // W[r][c], r = contraction index
             float v = 0.f;
             if (r < a.w && c < a.w) v = (a.gemm == GEMM_W) ? a.Wm[r * a.w + c] : a.Wm[c * a.w + r];
-            if constexpr (TC) Ws[boff<W>(c, r)] = tf32_rna(v);  // Bᵀ[n = c][k = r]
+            if constexpr (TC) Ws[boff<W>(c, r)] = v;  // Bᵀ[n = c][k = r]
             else Ws[i] = v;
         }
     }
@@ -518,7 +514,6 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
                         const float f = rfs[r];
                         v.x = __fmul_rn(f, v.x); v.y = __fmul_rn(f, v.y); v.z = __fmul_rn(f, v.z); v.w = __fmul_rn(f, v.w);
                     }
-                    if (do_gemm) { v.x = tf32_rna(v.x); v.y = tf32_rna(v.y); v.z = tf32_rna(v.z); v.w = tf32_rna(v.w); }
                     *reinterpret_cast<float4*>(Zs + zoff(r, c)) = v;
                 }
                 fence_proxy_async();
@@ -675,11 +670,12 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
                 for (int r = 0; r < TR; ++r) {
                     const float* gr = Et + r * ZLD + dn0;
                     float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3];
-                    if (TC && do_gemm) { g0 = tf32_rna(g0); g1 = tf32_rna(g1); g2 = tf32_rna(g2); g3 = tf32_rna(g3); }  // dW operands as the tensor core sees them
+                    if (TC && do_gemm) { g0 = tf32_op(g0); g1 = tf32_op(g1); g2 = tf32_op(g2); g3 = tf32_op(g3); }  // dW operands as the tensor core reads them
                     const float rf = (!TC && kScale) ? rfs[r] : 1.f;
 #pragma unroll
                     for (int i = 0; i < C::DMB; ++i) {
-                        const float z = TC ? Zs[zoff(r, dm0 + i)] : (kScale ? __fmul_rn(rf, Za[r * ZLD + dm0 + i]) : Za[r * ZLD + dm0 + i]);
+                        const float z = TC ? (do_gemm ? tf32_op(Zs[zoff(r, dm0 + i)]) : Zs[zoff(r, dm0 + i)])
+                                           : (kScale ? __fmul_rn(rf, Za[r * ZLD + dm0 + i]) : Za[r * ZLD + dm0 + i]);
                         t[i][0] = fmaf(z, g0, t[i][0]);
                         t[i][1] = fmaf(z, g1, t[i][1]);
                         t[i][2] = fmaf(z, g2, t[i][2]);

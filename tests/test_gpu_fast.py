@@ -2,7 +2,7 @@
 
 The GSR-C step in TF32 mode runs k_fast FWD / INV / BIN plus the k_hub
 pre-pass for rows longer than one aggregation segment. The oracle in TF32 mode
-(oracle.set_tf32) rounds the same operands the kernels round (cvt.rna), so the
+(oracle.set_tf32) truncates the same operands to TF32 that the tensor core does, so the
 two differ only by the tensor core's accumulation order; bounds as stated in
 tests/test_gpu_parity.py (TF32_ROW_RTOL per row for ≥ 99.5% of rows, masks
 ≥ 99.5% identical, TF32_GRAD_RTOL on one layer's parameter gradients,

@@ -254,9 +254,9 @@ def test_mem_peak_independent_of_depth(ctx, oracle):
     assert arena[(0, 64)] > arena[(0, 16)] > arena[(0, 4)]
 
 
-# TF32 mode: the kernel rounds both transform operands to TF32 (cvt.rna) and
-# the tcgen05 core sums w exact products; the oracle in TF32 mode
-# (oracle.set_tf32) applies the same rounding, so the two differ only by the
+# TF32 mode: the tensor core reads both transform operands as TF32 (low 13
+# mantissa bits truncated) and sums w exact products; the oracle in TF32 mode
+# (oracle.set_tf32) truncates the same operands, so the two differ only by the
 # accumulation order inside the tensor core (~1e-7 of a row's scale). A
 # difference that size can still flip a near-tie in a downstream GS top-k
 # mask, which swaps one selected column of that row. Stated TF32 bounds:

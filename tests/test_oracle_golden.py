@@ -136,13 +136,14 @@ def test_gs_topk_k_out_of_range(oracle):
     assert e.value.code == 1
 
 
-def test_oracle_tf32_rounding_rna(oracle):
-    """TF32 transform mode rounds operands to nearest, ties away (cvt.rna.tf32.f32)."""
+def test_oracle_tf32_operand_truncation(oracle):
+    """TF32 transform mode reads operands as the B200 tensor core does: the low
+    13 mantissa bits truncated (scratch/tf32_probe.cu measured 128/128)."""
     rp, ci = np.arange(2), np.arange(1)
     g = oracle.Graph(rp, ci, norm=0)
     W = np.ones((1, 1), np.float32)
-    cases = [(1 + 2.0 ** -11, 1 + 2.0 ** -10), (1 + 2.0 ** -12, 1.0), (-(1 + 2.0 ** -11), -(1 + 2.0 ** -10)),
-             (1 + 3 * 2.0 ** -12, 1 + 2.0 ** -10)]
+    cases = [(1 + 2.0 ** -11, 1.0), (1 + 2.0 ** -12, 1.0), (-(1 + 2.0 ** -11), -1.0), (1 + 3 * 2.0 ** -12, 1.0),
+             (1 + 2.0 ** -10 + 2.0 ** -11, 1 + 2.0 ** -10)]
     try:
         oracle.set_tf32(True)
         for x, want in cases:
