@@ -583,6 +583,227 @@ __global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_c
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
 }
 
+// ---- BIN with two threads per row --------------------------------------------
+// The dense transposed aggregation gathers a full neighbour row (4w bytes) per
+// edge; with one thread per row only one edge fits in registers at a time.
+// Here threads t and t + 128 share tile row t & 127, each owning one column
+// half: per thread an edge is w/8 float4 loads, two edges are in flight, and
+// the CTA has 8 warps. Everything else is the BIN kind of k_fast.
+template <int W>
+__device__ __forceinline__ void agg_dense_half(const FastArgs& a, int e0, int ne, float* Zs, int r, int hf) {
+    constexpr int HW = W / 2, NQ = HW / 4;
+    const bool unit = a.dir.unit_edge != 0;
+    const int cbase = hf * HW;
+    float acc[HW];
+#pragma unroll
+    for (int q = 0; q < HW; ++q) acc[q] = 0.f;
+    int u = 0;
+    int cn = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
+    int cn2 = ne > 1 ? __ldg(a.dir.idx + e0 + 1) : 0;
+#pragma unroll 1
+    for (; u < ne; u += 2) {  // two edges per round, CSR order kept in the adds
+        const int ca = cn, cb = cn2;
+        const bool hb = u + 1 < ne;
+        cn = u + 2 < ne ? __ldg(a.dir.idx + e0 + u + 2) : 0;
+        cn2 = u + 3 < ne ? __ldg(a.dir.idx + e0 + u + 3) : 0;
+        const float sa = unit ? 1.f : __ldg(a.dir.edge_f + ca);
+        const float sb = (unit || !hb) ? 1.f : __ldg(a.dir.edge_f + cb);
+        float4 xa[NQ], xb[NQ];
+        const float* pa = a.x_in + static_cast<size_t>(ca) * a.ld + cbase;
+        const float* pb = a.x_in + static_cast<size_t>(cb) * a.ld + cbase;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const bool ok = cbase + 4 * q < a.ld;
+            xa[q] = ok ? dev::ld4(pa + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            xb[q] = (ok && hb) ? dev::ld4(pb + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sa, xa[q].x));
+            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sa, xa[q].y));
+            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sa, xa[q].z));
+            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sa, xa[q].w));
+        }
+        if (hb) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sb, xb[q].x));
+                acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sb, xb[q].y));
+                acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sb, xb[q].z));
+                acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sb, xb[q].w));
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+        *reinterpret_cast<float4*>(Zs + zo(r, cbase + 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+}
+
+template <int W>
+__global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ FastArgs a) {
+    using Pl = Plan<W>;
+    constexpr int NT = 2 * TR, HW = W / 2;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* base = reinterpret_cast<float*>(smem_raw);
+    if ((smem_u32(base) & 1023u) != 0) __trap();
+    float* Ws = base;
+    float* Zs = Ws + Pl::ws;
+    float* Y2 = Zs + Pl::tile;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(BIN));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+    const int tid = threadIdx.x, wid = tid >> 5;
+    const int t = tid & (TR - 1), hf = tid >> 7;  // tile row, column half
+    const int c_lo = hf * HW;
+    const int n_tiles = (a.n + TR - 1) / TR;
+    constexpr uint32_t TCOLS = 2 * W < 64 ? 64 : 2 * W;
+
+    for (int i = tid; i < W * W; i += NT) {  // Bᵀ[n][m] = W[n][m] (h = Y·Wᵀ)
+        const int r = i / W, c = i % W;
+        Ws[tile::boff<W>(c, r)] = (r < a.w && c < a.w) ? a.Wm[c * a.w + r] : 0.f;
+    }
+    if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
+    if (wid == 0) tile::tmem_alloc(tslot, TCOLS);
+    tile::fence_proxy_async();
+    tile::tc_fence_before();
+    __syncthreads();
+    tile::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tlane = static_cast<uint32_t>(32 * (wid & 3)) << 16;
+    uint32_t ph0 = 0, ph1 = 0;
+    bool dw_pending = false;
+
+    for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
+        const int row0 = tile_i * TR, row = row0 + t;
+        const bool valid = row < a.n;
+        if (dw_pending) {
+            mbar_wait(&bar[1], ph1);
+            ph1 ^= 1u;
+            tile::tc_fence_after();
+            dw_pending = false;
+        }
+        // ---- Y = Âᵀ·x_in: this thread's column half of row t
+        float rf = 0.f;
+        if (valid) {
+            const int e0 = __ldg(a.dir.ptr + row), ne = __ldg(a.dir.ptr + row + 1) - e0;
+            rf = __ldg(a.dir.out_f + row);
+            if (ne > kSegF) {
+                const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
+#pragma unroll
+                for (int c = 0; c < HW; c += 4)
+                    *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c)) = c_lo + c < a.ld ? dev::ld4(zh + c_lo + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                agg_dense_half<W>(a, e0, ne, Zs, t, hf);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int c = 0; c < HW; c += 4) {  // Â scale; Y2 = Y in BASE32B for dW
+            float4* p = reinterpret_cast<float4*>(Zs + zo(t, c_lo + c));
+            float4 v = *p;
+            v.x = __fmul_rn(rf, v.x); v.y = __fmul_rn(rf, v.y); v.z = __fmul_rn(rf, v.z); v.w = __fmul_rn(rf, v.w);
+            *p = v;
+            *reinterpret_cast<float4*>(Y2 + zb(t, c_lo + c)) = v;
+        }
+        tile::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tile::tc_fence_after();
+            const uint32_t za = smem_u32(Zs), wa = smem_u32(Ws);
+#pragma unroll
+            for (int kk = 0; kk < W / 8; ++kk)
+                umma(tmem, desc_sw128(za + (kk >> 2) * (TR * 128) + (kk & 3) * 32, 16), desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16),
+                     idesc<W>(0, 0), kk > 0 ? 1u : 0u);
+            tile::umma_commit(&bar[0]);
+        }
+        // mask record of the row (the block's input records: S and the input-gradient mask)
+        uint32_t iw[4] = {0u, 0u, 0u, 0u};
+        const uint8_t* rc = a.mrec + static_cast<size_t>(valid ? row : 0) * rec_bytes(a.k_m);
+        if (valid) {
+            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
+            iw[0] = iw4.x; iw[1] = iw4.y; iw[2] = iw4.z; iw[3] = iw4.w;
+        }
+        mbar_wait(&bar[0], ph0);
+        ph0 ^= 1u;
+        tile::tc_fence_after();
+        // ---- h = Y·Wᵀ (this thread's half) → Zs, for the masked scatter
+#pragma unroll
+        for (int c0 = 0; c0 < HW; c0 += 16) {
+            float h[16];
+            tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(c_lo + c0), h);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4)
+                *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c0 + q)) = make_float4(h[q], h[q + 1], h[q + 2], h[q + 3]);
+        }
+        // ---- dst_p[r, c] += h[r, c] for the mask columns in this half (distinct
+        // columns: loads first, then stores)
+        if (valid) {
+            int col[16];
+            float v[16];
+            bool mine[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                col[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                mine[j] = j < a.k_m && (col[j] / HW) == hf;
+                v[j] = mine[j] ? Zs[zo(t, col[j])] : 0.f;
+            }
+            for (int p = 0; p < a.ndst; ++p) {
+                float* d = a.dst[p] + static_cast<size_t>(row) * a.ld;
+                float o[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) if (mine[j]) o[j] = d[col[j]];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) if (mine[j]) d[col[j]] = __fadd_rn(o[j], v[j]);
+            }
+        }
+        // ---- S = scatter(V, I) of the row over its h half (BASE32B): dW += Sᵀ·Y
+#pragma unroll
+        for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(Zs + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            const float* rv = reinterpret_cast<const float*>(rc + rec_kh(a.k_m));
+            for (int j = 0; j < a.k_m; ++j) {
+                const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                if (c / HW == hf) Zs[zb(t, c)] = __ldg(rv + j);
+            }
+        }
+        tile::fence_proxy_async();
+        tile::tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tile::tc_fence_after();
+            const uint32_t sa = smem_u32(Zs), ya = smem_u32(Y2);
+            const bool first = tile_i == static_cast<int>(blockIdx.x);
+#pragma unroll
+            for (int kk = 0; kk < TR / 8; ++kk)
+                umma(tmem + W, desc_mn32(sa + kk * 1024), desc_mn32(ya + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
+            tile::umma_commit(&bar[1]);
+        }
+        dw_pending = true;
+    }
+    if (dw_pending) {
+        mbar_wait(&bar[1], ph1);
+        tile::tc_fence_after();
+    }
+    // per-CTA dW partial: TMEM lane m, columns W + n; each half writes its columns
+    const int plen = a.w * a.w + a.w;
+    double* pp = a.part + static_cast<size_t>(blockIdx.x) * plen;
+#pragma unroll
+    for (int c0 = 0; c0 < HW; c0 += 16) {
+        float v[16];
+        tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(W + c_lo + c0), v);
+        if (t < a.w) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c_lo + c0 + j < a.w) pp[t * a.w + c_lo + c0 + j] = static_cast<double>(v[j]);
+        }
+    }
+    if (hf == 0 && t < a.w) pp[a.w * a.w + t] = 0.0;  // db: k_colsum (bias only)
+    tile::tc_fence_before();
+    __syncthreads();
+    if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
+}
+
 // ---- hub rows (deg > kSeg): canonical segmented sums, one CTA per row --------
 // Segments of kSeg edges are summed from +0 (thread per segment for records,
 // warp per segment for dense rows) into shared slots, then folded left to
@@ -739,10 +960,42 @@ cudaError_t set_attr() {
 }
 
 template <int W>
+int occupancy_bin2() {
+    static int occ = 0;
+    if (!occ) {
+        int dev = 0, smem_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k_bin2<W>);
+        const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(BIN) + 1024);
+        const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
+        const int by_regs = 65536 / (regs * 2 * TR);
+        occ = by_smem < by_regs ? by_smem : by_regs;
+        const int tcols = 2 * W < 64 ? 64 : 2 * W;
+        if (occ > 512 / tcols) occ = 512 / tcols;
+        if (occ < 1) occ = 1;
+    }
+    return occ;
+}
+
+template <int W>
+cudaError_t launch_bin2(const FastArgs& a, cudaStream_t s, int* grid_out) {
+    const int tiles = (a.n + TR - 1) / TR;
+    const int cap = tile::sm_count_host() * occupancy_bin2<W>();
+    const int grid = tiles < cap ? tiles : cap;
+    if (grid_out) *grid_out = grid;
+    if (grid == 0) return cudaSuccess;
+    k_bin2<W><<<grid, 2 * TR, Plan<W>::bytes(BIN), s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int W>
 cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {set_attr<W, FWD, 0>(), set_attr<W, FWD, 8>(), set_attr<W, FWD, 16>(), set_attr<W, INV, 0>(), set_attr<W, INV, 8>(),
-                          set_attr<W, INV, 16>(), set_attr<W, BIN, 0>()})
+                          set_attr<W, INV, 16>(), set_attr<W, BIN, 0>(),
+                          cudaFuncSetAttribute(k_bin2<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
         if (r != cudaSuccess) e = r;
     return e;
 }
@@ -761,7 +1014,7 @@ cudaError_t launch_w(int kind, const FastArgs& a, cudaStream_t s, int* g) {
     switch (kind) {
         case FWD: return launch_k<W, FWD>(a, s, g);
         case INV: return launch_k<W, INV>(a, s, g);
-        default: return launch<W, BIN, 0>(a, s, g);
+        default: return launch_bin2<W>(a, s, g);
     }
 }
 
