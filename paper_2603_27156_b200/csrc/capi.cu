@@ -144,7 +144,7 @@ struct gsrc_ctx {
     // activation arena
     Arena arena;
     float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr, *Zh = nullptr;
-    std::vector<CUtensorMap> xmaps;  // TMA maps of the X planes (fast path)
+    std::vector<CUtensorMap> xmaps, gmaps;  // TMA maps of the X and G planes (fast path)
     uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
     std::vector<uint8_t*> c1, c2;
     std::vector<char> filled;
@@ -312,8 +312,11 @@ struct gsrc_ctx {
         b.mrec = rec;
         b.k_m = k;
         b.part = part;
-        if (i > 0) { b.dst[0] = plane(G, i - 1); b.ndst = 1; }
-        else { for (int p = 1; p < C; ++p) b.dst[p - 1] = plane(G, p); b.ndst = C - 1; }
+        if (i > 0) { b.dst[0] = plane(G, i - 1); b.tm_dst[0] = gmaps[static_cast<size_t>(i - 1)]; b.ndst = 1; }
+        else {
+            for (int p = 1; p < C; ++p) { b.dst[p - 1] = plane(G, p); b.tm_dst[p - 1] = gmaps[static_cast<size_t>(p)]; }
+            b.ndst = C - 1;
+        }
         run_fast(2, b);
     }
 
@@ -548,8 +551,12 @@ struct gsrc_ctx {
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
         Zh = fast() ? arena.lease<float>(pl) : nullptr;
         xmaps.assign(static_cast<size_t>(C), CUtensorMap{});
+        gmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         if (fast())
-            for (int p = 0; p < C; ++p) CK(encode_plane_map(&xmaps[static_cast<size_t>(p)], plane(X, p), static_cast<int>(n), ld));
+            for (int p = 0; p < C; ++p) {
+                CK(encode_plane_map(&xmaps[static_cast<size_t>(p)], plane(X, p), static_cast<int>(n), ld));
+                CK(encode_plane_map(&gmaps[static_cast<size_t>(p)], plane(G, p), static_cast<int>(n), ld));
+            }
         c1.clear();
         c2.clear();
         if (alg12) {

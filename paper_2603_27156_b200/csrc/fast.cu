@@ -95,6 +95,10 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
                  ::"l"(m), "r"(c0), "r"(r0), "r"(smem_u32(src)) : "memory");
 }
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int c0, int r0) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(m), "r"(c0), "r"(r0), "r"(smem_u32(src)) : "memory");
+}
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -719,53 +723,57 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
         }
         // mask record of the row (the block's input records: S and the input-gradient mask)
         uint32_t iw[4] = {0u, 0u, 0u, 0u};
-        const uint8_t* rc = a.mrec + static_cast<size_t>(valid ? row : 0) * rec_bytes(a.k_m);
+        float rv[16];
         if (valid) {
+            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
             const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
             iw[0] = iw4.x; iw[1] = iw4.y; iw[2] = iw4.z; iw[3] = iw4.w;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v4 = 4 * q < a.k_m ? *reinterpret_cast<const float4*>(rc + 16 + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                rv[4 * q] = v4.x; rv[4 * q + 1] = v4.y; rv[4 * q + 2] = v4.z; rv[4 * q + 3] = v4.w;
+            }
+        }
+        // this half's mask columns as a bitmask (mask of a padding / invalid row: empty)
+        uint32_t hm = 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+            if (valid && j < a.k_m && c / HW == hf) hm |= 1u << (c - c_lo);
         }
         mbar_wait(&bar[0], ph0);
         ph0 ^= 1u;
         tile::tc_fence_after();
-        // ---- h = Y·Wᵀ (this thread's half) → Zs, for the masked scatter
+        // ---- du = mask ⊙ (Y·Wᵀ), this thread's half → Zs: the tile TMA
+        // reduce-adds into every destination plane (each element receives one
+        // add, so the result is deterministic; off-mask entries add +0)
 #pragma unroll
         for (int c0 = 0; c0 < HW; c0 += 16) {
             float h[16];
             tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(c_lo + c0), h);
 #pragma unroll
+            for (int q = 0; q < 16; ++q) h[q] = (hm >> (c0 + q)) & 1u ? h[q] : 0.f;
+#pragma unroll
             for (int q = 0; q < 16; q += 4)
                 *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c0 + q)) = make_float4(h[q], h[q + 1], h[q + 2], h[q + 3]);
         }
-        // ---- dst_p[r, c] += h[r, c] for the mask columns in this half (distinct
-        // columns: loads first, then stores)
-        if (valid) {
-            int col[16];
-            float v[16];
-            bool mine[16];
+        tile::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            for (int p = 0; p < a.ndst; ++p)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                col[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                mine[j] = j < a.k_m && (col[j] / HW) == hf;
-                v[j] = mine[j] ? Zs[zo(t, col[j])] : 0.f;
-            }
-            for (int p = 0; p < a.ndst; ++p) {
-                float* d = a.dst[p] + static_cast<size_t>(row) * a.ld;
-                float o[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) if (mine[j]) o[j] = d[col[j]];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) if (mine[j]) d[col[j]] = __fadd_rn(o[j], v[j]);
-            }
+                for (int c = 0; c < W; c += 32) tma_reduce_add_2d(&a.tm_dst[p], Zs + (c >> 5) * (TR * 32), c, row0);
+            tma_store_commit();
+            tma_store_wait_read();  // Zs is rewritten with S below
         }
-        // ---- S = scatter(V, I) of the row over its h half (BASE32B): dW += Sᵀ·Y
+        __syncthreads();
+        // ---- S = scatter(V, I) of the row (BASE32B): dW += Sᵀ·Y
 #pragma unroll
         for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(Zs + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) {
-            const float* rv = reinterpret_cast<const float*>(rc + rec_kh(a.k_m));
-            for (int j = 0; j < a.k_m; ++j) {
-                const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                if (c / HW == hf) Zs[zb(t, c)] = __ldg(rv + j);
-            }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+            if (valid && j < a.k_m && c / HW == hf) Zs[zb(t, c)] = rv[j];
         }
         tile::fence_proxy_async();
         tile::tc_fence_before();

@@ -107,6 +107,7 @@ struct FastArgs {
     float* dst[kMaxDst] = {};
     int ndst = 0;
     CUtensorMap tm_x;                      // FWD / INV: 2-D tiled map of the R/out plane (128 rows × 32 cols, SWIZZLE_128B)
+    CUtensorMap tm_dst[kMaxDst];           // BIN: maps of the dst planes (TMA reduce-add of the masked gradient tile)
 };
 
 bool fast_supported(int w, int k);
