@@ -122,6 +122,10 @@ struct gsrc_ctx {
     float *row_f = nullptr, *col_f = nullptr;
     int *hub_f = nullptr, *hub_b = nullptr;   // rows with > kSeg edges (fwd CSR / transpose), fast path
     int nhub_f = 0, nhub_b = 0;
+    // their kSeg-edge segments (edge ranges) and each hub row's segment range
+    int2 *seg_f = nullptr, *seg_b = nullptr;
+    int *segoff_f = nullptr, *segoff_b = nullptr;
+    int nseg_f = 0, nseg_b = 0;
     size_t graph_bytes = 0;
 
     // persistent: model state
@@ -167,7 +171,8 @@ struct gsrc_ctx {
     ~gsrc_ctx() {
         if (g_fb) cudaGraphExecDestroy(g_fb);
         if (g_step) cudaGraphExecDestroy(g_step);
-        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)params, (void*)grads,
+        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)seg_f, (void*)seg_b,
+                        (void*)segoff_f, (void*)segoff_b, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
@@ -256,11 +261,13 @@ struct gsrc_ctx {
         f.Zh = Zh;
         return f;
     }
+    float* Pseg = nullptr;  // hub segment partials (arena)
     void run_hub(bool sparse, const FastArgs& f, bool transpose) {
         const int nh = transpose ? nhub_b : nhub_f;
         if (!nh) return;
-        CK(launch_hub(sparse, f, transpose ? hub_b : hub_f, nh, stream));
-        ++launches;
+        CK(launch_hub_segs(sparse, f, transpose ? seg_b : seg_f, transpose ? nseg_b : nseg_f, transpose ? hub_b : hub_f,
+                           transpose ? segoff_b : segoff_f, nh, Pseg, stream));
+        launches += 2;
     }
     void run_fast(int kind, const FastArgs& f) {
         CK(launch_fast(kind, f, stream, &last_grid));
@@ -536,6 +543,8 @@ struct gsrc_ctx {
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
         if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
         if (fast()) total += bytes_rounded(pl * sizeof(float));            // Zh (hub-row aggregates)
+        const size_t nsegmax = static_cast<size_t>(std::max(nseg_f, nseg_b));
+        if (fast()) total += bytes_rounded(std::max<size_t>(nsegmax, 1) * ld * sizeof(float));  // Pseg
         if (alg12) total += 2 * bytes_rounded(pl * sizeof(float)) + 3 * bytes_rounded(rb) + 2 * static_cast<size_t>(cfg.layers) * bytes_rounded(rb);
         arena.plan(total);
         X = arena.lease<float>(pl * C);
@@ -550,6 +559,7 @@ struct gsrc_ctx {
         U = nullptr;
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
         Zh = fast() ? arena.lease<float>(pl) : nullptr;
+        Pseg = fast() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
         xmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         gmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         if (fast())
@@ -744,13 +754,31 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
-        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b}) if (p) cudaFree(p);
+        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b, (void*)ctx->seg_f, (void*)ctx->seg_b, (void*)ctx->segoff_f, (void*)ctx->segoff_b})
+            if (p) cudaFree(p);
         ctx->nhub_f = static_cast<int>(hf.size());
         ctx->nhub_b = static_cast<int>(hb.size());
         ctx->hub_f = dmalloc<int>(hf.size(), &ctx->graph_bytes);
         ctx->hub_b = dmalloc<int>(hb.size(), &ctx->graph_bytes);
         if (!hf.empty()) CK(cudaMemcpy(ctx->hub_f, hf.data(), sizeof(int) * hf.size(), cudaMemcpyHostToDevice));
         if (!hb.empty()) CK(cudaMemcpy(ctx->hub_b, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
+        auto seg_table = [&](const std::vector<int>& hubs, const std::vector<int>& ptr, int2*& segs, int*& off, int& nseg) {
+            std::vector<int2> sv;
+            std::vector<int> ov(hubs.size() + 1, 0);
+            for (size_t h = 0; h < hubs.size(); ++h) {
+                ov[h] = static_cast<int>(sv.size());
+                const int e0 = ptr[static_cast<size_t>(hubs[h])], e1 = ptr[static_cast<size_t>(hubs[h]) + 1];
+                for (int lo = e0; lo < e1; lo += kAggSeg) sv.push_back(make_int2(lo, std::min(e1, lo + kAggSeg)));
+            }
+            ov[hubs.size()] = static_cast<int>(sv.size());
+            nseg = static_cast<int>(sv.size());
+            segs = dmalloc<int2>(sv.size(), &ctx->graph_bytes);
+            off = dmalloc<int>(ov.size(), &ctx->graph_bytes);
+            if (!sv.empty()) CK(cudaMemcpy(segs, sv.data(), sizeof(int2) * sv.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(off, ov.data(), sizeof(int) * ov.size(), cudaMemcpyHostToDevice));
+        };
+        seg_table(hf, rp, ctx->seg_f, ctx->segoff_f, ctx->nseg_f);
+        seg_table(hb, trp, ctx->seg_b, ctx->segoff_b, ctx->nseg_b);
         CK(cudaDeviceSynchronize());  // pageable copies may still be in flight when cudaMemcpy returns
         const bool resize = ctx->n != n;
         ctx->n = n;
@@ -758,7 +786,7 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         ctx->norm = norm;
         ctx->drop_graphs();
         if (resize) ctx->data = false;
-        if (resize && ctx->model) ctx->plan_arena();  // node count changed: re-plan activations
+        if (ctx->model) ctx->plan_arena();  // node count / hub segments changed: re-plan activations
     });
 }
 

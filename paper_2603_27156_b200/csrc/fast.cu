@@ -812,107 +812,139 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
 }
 
-// ---- hub rows (deg > kSeg): canonical segmented sums, one CTA per row --------
-// Segments of kSeg edges are summed from +0 (thread per segment for records,
-// warp per segment for dense rows) into shared slots, then folded left to
-// right per column — the oracle's aggregation order for long rows.
-template <int W, bool SPARSE>
-__global__ void __launch_bounds__(SPARSE ? 64 : 128) k_hub(FastArgs a, const int* __restrict__ hubs) {
-    constexpr int NS = SPARSE ? 64 : 16;  // segments per round
-    constexpr int PL = W + 4;  // 16 B aligned slot rows
-    __shared__ __align__(16) float P[NS * PL];
-    const int r = __ldg(hubs + blockIdx.x);
+// ---- hub rows (deg > kSeg), flattened over segments ---------------------------
+// Canonical order for a long row: kSeg-edge segments, each summed from +0 in
+// CSR order, then folded left to right. Pass 1 computes every hub segment of
+// the graph independently (one warp per segment, lanes over columns — dense —
+// or over record slots — sparse), writing its partial row to Pseg; pass 2
+// folds each hub row's partials in order (one warp per row, coalesced rows).
+// Work is spread over all SMs regardless of how skewed the hub degrees are.
+constexpr int kHubSegThreads = 64;
+template <int W>
+__global__ void __launch_bounds__(kHubSegThreads) k_hub_seg_sparse(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
+    // one thread per segment: ≤ 8 records, 128-bit loads one record ahead, scattered
+    // into a private shared row; the block's rows then leave as coalesced warp stores
+    constexpr int PL = W + 4;
+    __shared__ __align__(16) float slot[kHubSegThreads * PL];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int e0 = __ldg(a.dir.ptr + r), e1 = __ldg(a.dir.ptr + r + 1);
-    const int nseg = (e1 - e0 + kSegF - 1) / kSegF;
-    const bool unit = a.dir.unit_edge != 0;
-    float z = 0.f;  // thread t < W: running fold of column t
-    for (int h0 = 0; h0 < nseg; h0 += NS) {
-        const int nr = min(NS, nseg - h0);
-        if constexpr (SPARSE) {
-            if (t < nr) {
-                float* pr = P + t * PL;
+    const int sgi = blockIdx.x * kHubSegThreads + t;
+    float* pr = slot + t * PL;
 #pragma unroll
-                for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int lo = e0 + (h0 + t) * kSegF, ne = min(e1, lo + kSegF) - lo;
-                const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
-                int cs[kSegF];
+    for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sgi < nseg) {
+        const int2 se = __ldg(segs + sgi);
+        const int lo = se.x, ne = se.y - se.x;
+        const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
+        const bool unit = a.dir.unit_edge != 0;
+        int cs[kSegF];
 #pragma unroll
-                for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
+        for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
 #pragma unroll
-                for (int u = 1; u < kSegF; ++u)
-                    if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
-                tile::SparseRec buf[2];
-                tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
+        for (int u = 1; u < kSegF; ++u)
+            if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
+        tile::SparseRec buf[2];
+        tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
 #pragma unroll
-                for (int u = 0; u < kSegF; ++u) {
-                    if (u < ne) {
-                        if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
-                        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
-                        const tile::SparseRec& rc = buf[u & 1];
-                        const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
-                        const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
-                                              rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
-                        float old[16];
-                        int mm[16];
+        for (int u = 0; u < kSegF; ++u) {
+            if (u < ne) {
+                if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
+                const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
+                const tile::SparseRec& rc = buf[u & 1];
+                const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
+                const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
+                                      rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
+                int mm[16];
+                float old[16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            mm[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                            if (j < k) old[j] = pr[mm[j]];
-                        }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (j < k) pr[mm[j]] = __fadd_rn(old[j], unit ? vv[j] : __fmul_rn(sc, vv[j]));
-                    }
+                for (int j = 0; j < 16; ++j) {
+                    mm[j] = static_cast<int>(__byte_perm(iw[j >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
+                    if (j < k) old[j] = pr[mm[j]];
                 }
-            }
-        } else {
-            constexpr int CPL = W / 32 > 0 ? W / 32 : 1;
-            for (int s = wid; s < nr; s += 4) {
-                const int lo = e0 + (h0 + s) * kSegF, ne = min(e1, lo + kSegF) - lo;
-                float x[kSegF][CPL];
 #pragma unroll
-                for (int u = 0; u < kSegF; ++u) {  // all of the segment's row loads in flight
-                    const int c = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        const int col = lane + 32 * q;
-                        x[u][q] = (u < ne && col < a.ld) ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
-                    }
-                    if (!unit && u < ne) {
-                        const float sc = __ldg(a.dir.edge_f + c);
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) x[u][q] = __fmul_rn(sc, x[u][q]);
-                    }
-                }
-                float acc[CPL];
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
-#pragma unroll
-                for (int u = 0; u < kSegF; ++u)
-                    if (u < ne)
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) acc[q] = __fadd_rn(acc[q], x[u][q]);
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) if (lane + 32 * q < W) P[s * PL + lane + 32 * q] = acc[q];
+                for (int j = 0; j < 16; ++j)
+                    if (j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
             }
         }
-        __syncthreads();
-        if (t < W) {
-            int i = 0;
-            if (h0 == 0) { z = P[t]; i = 1; }
-            for (; i + 8 <= nr; i += 8) {  // independent loads, then the ordered fold
-                float pv[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) pv[q] = P[(i + q) * PL + t];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) z = __fadd_rn(z, pv[q]);
-            }
-            for (; i < nr; ++i) z = __fadd_rn(z, P[i * PL + t]);
-        }
-        __syncthreads();
     }
-    if (t < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + t] = z;
+    __syncwarp();
+    for (int i = 0; i < 32; ++i) {  // warp copies its 32 partial rows out, lanes over columns
+        const int sg = blockIdx.x * kHubSegThreads + wid * 32 + i;
+        if (sg >= nseg) break;
+        const float* src = slot + (wid * 32 + i) * PL;
+        for (int c = lane; c < a.ld; c += 32) Pseg[static_cast<size_t>(sg) * a.ld + c] = src[c];
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_hub_seg_dense(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
+    // one warp per segment, lanes over columns: every neighbour row is one coalesced load
+    constexpr int CPL = W / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int sgi = blockIdx.x * 8 + wid;
+    if (sgi >= nseg) return;
+    const int2 se = __ldg(segs + sgi);
+    const int lo = se.x, ne = se.y - se.x;
+    const bool unit = a.dir.unit_edge != 0;
+    const int myc = lane < ne ? __ldg(a.dir.idx + lo + lane) : 0;
+    const float mysc = (!unit && lane < ne) ? __ldg(a.dir.edge_f + myc) : 1.f;
+    float x[kSegF][CPL];
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) {
+        const int c = __shfl_sync(0xffffffffu, myc, u);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+            const int col = lane + 32 * q;
+            x[u][q] = (u < ne && col < a.ld) ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
+        }
+    }
+    float acc[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+#pragma unroll
+    for (int u = 0; u < kSegF; ++u) {
+        const float sc = __shfl_sync(0xffffffffu, mysc, u);
+        if (u < ne)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(sc, x[u][q]));
+    }
+    float* out = Pseg + static_cast<size_t>(sgi) * a.ld;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+        if (lane + 32 * q < a.ld) out[lane + 32 * q] = acc[q];
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_hub_fold(FastArgs a, const int* __restrict__ rows, const int* __restrict__ seg_off, int nhub,
+                                                  const float* __restrict__ Pseg) {
+    constexpr int CPL = W / 32;
+    const int lane = threadIdx.x & 31;
+    const int h = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (h >= nhub) return;
+    const int s0 = __ldg(seg_off + h), s1 = __ldg(seg_off + h + 1);
+    float z[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) z[q] = (lane + 32 * q < a.ld) ? __ldg(Pseg + static_cast<size_t>(s0) * a.ld + lane + 32 * q) : 0.f;
+    int s = s0 + 1;
+    for (; s + 8 <= s1; s += 8) {  // eight partial rows in flight, folded in order
+        float p[8][CPL];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+                p[i][q] = (lane + 32 * q < a.ld) ? __ldg(Pseg + static_cast<size_t>(s + i) * a.ld + lane + 32 * q) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) z[q] = __fadd_rn(z[q], p[i][q]);
+    }
+    for (; s < s1; ++s)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+            z[q] = __fadd_rn(z[q], (lane + 32 * q < a.ld) ? __ldg(Pseg + static_cast<size_t>(s) * a.ld + lane + 32 * q) : 0.f);
+    const int r = __ldg(rows + h);
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+        if (lane + 32 * q < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + lane + 32 * q] = z[q];
 }
 
 // db = colsum(G) (bias only): per-CTA partials over 128-row tiles in row
@@ -1026,13 +1058,6 @@ cudaError_t launch_w(int kind, const FastArgs& a, cudaStream_t s, int* g) {
     }
 }
 
-template <int W>
-cudaError_t launch_hub_w(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {
-    if (sparse) k_hub<W, true><<<nhub, 64, 0, s>>>(a, hubs);  // thread per segment, W ≤ 64 fold threads
-    else k_hub<W, false><<<nhub, 128, 0, s>>>(a, hubs);
-    return cudaGetLastError();
-}
-
 }  // namespace fast
 
 cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld) {
@@ -1075,6 +1100,24 @@ cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_o
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_hub_segs(bool sparse, const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub,
+                            float* Pseg, cudaStream_t s) {
+    if (nhub == 0) return cudaSuccess;
+    const int gsp = (nseg + fast::kHubSegThreads - 1) / fast::kHubSegThreads, gsd = (nseg + 7) / 8, gf = (nhub + 7) / 8;
+    if (a.w <= 32) {
+        if (sparse) fast::k_hub_seg_sparse<32><<<gsp, fast::kHubSegThreads, 0, s>>>(a, segs, nseg, Pseg);
+        else fast::k_hub_seg_dense<32><<<gsd, 256, 0, s>>>(a, segs, nseg, Pseg);
+        fast::k_hub_fold<32><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
+    } else if (a.w <= 64) {
+        if (sparse) fast::k_hub_seg_sparse<64><<<gsp, fast::kHubSegThreads, 0, s>>>(a, segs, nseg, Pseg);
+        else fast::k_hub_seg_dense<64><<<gsd, 256, 0, s>>>(a, segs, nseg, Pseg);
+        fast::k_hub_fold<64><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
+    } else {
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, int* grid_out, cudaStream_t s) {
     const int tiles = (n + fast::TR - 1) / fast::TR;
     const int cap = tile::sm_count_host() * 8;
@@ -1084,11 +1127,5 @@ cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s) {
-    if (nhub == 0) return cudaSuccess;
-    if (a.w <= 32) return fast::launch_hub_w<32>(sparse, a, hubs, nhub, s);
-    if (a.w <= 64) return fast::launch_hub_w<64>(sparse, a, hubs, nhub, s);
-    return cudaErrorInvalidValue;
-}
 
 }  // namespace gsrk

@@ -116,7 +116,9 @@ bool fast_supported(int w, int k);
 cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld);
 cudaError_t init_fast_attributes();
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out);
-cudaError_t launch_hub(bool sparse, const FastArgs& a, const int* hubs, int nhub, cudaStream_t s);
+// hub rows flattened over their kSeg-edge segments: partials, then ordered fold
+cudaError_t launch_hub_segs(bool sparse, const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub,
+                            float* Pseg, cudaStream_t s);
 cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, int* grid_out, cudaStream_t s);
 
 // GS top-k of (sum of) planes: u = p0 + p1 + ... (left to right), records out.
