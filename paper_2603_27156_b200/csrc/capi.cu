@@ -205,6 +205,23 @@ struct gsrc_ctx {
         CK(launch_tile(a, stream, &last_grid));
         ++launches;
     }
+    // TMA map of an activation / gradient plane (fast path), nullptr otherwise
+    const CUtensorMap* map_of(const float* p) const {
+        for (int q = 0; q < C && q < static_cast<int>(xmaps.size()); ++q) {
+            if (p == plane(X, q)) return &xmaps[static_cast<size_t>(q)];
+            if (p == plane(G, q)) return &gmaps[static_cast<size_t>(q)];
+        }
+        return nullptr;
+    }
+    void launch_gs_any(GsArgs& g) {
+        bool tma = fast();
+        for (int i = 0; i < g.nplanes && tma; ++i) {
+            const CUtensorMap* m = map_of(g.planes[i]);
+            if (m) g.maps[i] = *m; else tma = false;
+        }
+        CK(tma ? launch_gs_tma(g, stream) : launch_gs(g, stream));
+        ++launches;
+    }
     void run_gs(std::initializer_list<const float*> planes, uint8_t* rec) {
         GsArgs g;
         g.n = static_cast<int>(n);
@@ -215,8 +232,7 @@ struct gsrc_ctx {
         for (const float* p : planes) g.planes[i++] = p;
         g.nplanes = i;
         g.rec = rec;
-        CK(launch_gs(g, stream));
-        ++launches;
+        launch_gs_any(g);
     }
     void run_gs_groupsum(const float* base, uint8_t* rec) {  // GS(Σ_{j≥2} x_j), planes 1..C-1
         GsArgs g;
@@ -227,8 +243,7 @@ struct gsrc_ctx {
         for (int p = 1; p < C; ++p) g.planes[p - 1] = plane(const_cast<float*>(base), p);
         g.nplanes = C - 1;
         g.rec = rec;
-        CK(launch_gs(g, stream));
-        ++launches;
+        launch_gs_any(g);
     }
     void run_sum_planes(const float* base, float* out) {
         GsArgs g;

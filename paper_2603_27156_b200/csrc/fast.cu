@@ -947,6 +947,60 @@ __global__ void __launch_bounds__(256) k_hub_fold(FastArgs a, const int* __restr
         if (lane + 32 * q < a.ld) a.Zh[static_cast<size_t>(r) * a.ld + lane + 32 * q] = z[q];
 }
 
+// ---- GS top-k of planes (backward recompute, Eq. 6 group sum) ---------------
+// u = p0 + p1 + … (left to right) per row, then GS_k(u) → records. Plane
+// tiles (128 rows × W) arrive by TMA into two alternating shared buffers (the
+// next tile's load overlaps this one's selection); thread t owns row t.
+template <int W>
+__global__ void __launch_bounds__(TR, 3) k_gs_tma(const __grid_constant__ GsArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* buf = reinterpret_cast<float*>(smem_raw);
+    if ((smem_u32(buf) & 1023u) != 0) __trap();
+    uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * TR * W);
+    const int t = threadIdx.x;
+    const int n_tiles = (a.n + TR - 1) / TR;
+    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int nl = my_tiles * a.nplanes;  // this CTA's loads: (tile, plane) in order
+    if (t == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
+    __syncthreads();
+    auto issue = [&](int j) {
+        const int tile_i = blockIdx.x + (j / a.nplanes) * gridDim.x, p = j % a.nplanes;
+        float* dst = buf + (j & 1) * TR * W;
+        mbar_expect_tx(&bar[j & 1], static_cast<uint32_t>(TR * W * 4));
+#pragma unroll
+        for (int c = 0; c < W; c += 32) tma_load_2d(&a.maps[p], dst + (c >> 5) * (TR * 32), &bar[j & 1], c, tile_i * TR);
+    };
+    if (t == 0 && nl > 0) issue(0);
+    uint32_t ph[2] = {0u, 0u};
+    float acc[W];
+    for (int j = 0; j < nl; ++j) {
+        if (t == 0 && j + 1 < nl) issue(j + 1);  // the other buffer was released by the barrier below
+        mbar_wait(&bar[j & 1], ph[j & 1]);
+        ph[j & 1] ^= 1u;
+        float* Ts = buf + (j & 1) * TR * W;
+        const int tile_i = blockIdx.x + (j / a.nplanes) * gridDim.x, p = j % a.nplanes;
+        const int row = tile_i * TR + t;
+        if (a.nplanes > 1) {
+#pragma unroll
+            for (int c = 0; c < W; c += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(Ts + zo(t, c));
+                if (p == 0) { acc[c] = v.x; acc[c + 1] = v.y; acc[c + 2] = v.z; acc[c + 3] = v.w; }
+                else {
+                    acc[c] = __fadd_rn(acc[c], v.x); acc[c + 1] = __fadd_rn(acc[c + 1], v.y);
+                    acc[c + 2] = __fadd_rn(acc[c + 2], v.z); acc[c + 3] = __fadd_rn(acc[c + 3], v.w);
+                }
+            }
+            if (p == a.nplanes - 1) {  // the sum goes back into this thread's row for the selection
+#pragma unroll
+                for (int c = 0; c < W; c += 4)
+                    *reinterpret_cast<float4*>(Ts + zo(t, c)) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            }
+        }
+        if (p == a.nplanes - 1 && row < a.n) gs_row<W, 16>(Ts, t, a.w, a.k, a.rec + static_cast<size_t>(row) * rec_bytes(a.k));
+        __syncthreads();
+    }
+}
+
 // db = colsum(G) (bias only): per-CTA partials over 128-row tiles in row
 // order (float within a tile, double across tiles), reduced in fixed order.
 __global__ void __launch_bounds__(128) k_colsum(const float* __restrict__ G, int n, int w, int ld, double* __restrict__ part) {
@@ -1085,7 +1139,9 @@ bool fast_supported(int w, int k) { return w >= 1 && w <= 64 && k >= 1 && k <= 1
 
 cudaError_t init_fast_attributes() {
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {fast::set_attrs<32>(), fast::set_attrs<64>()})
+    for (cudaError_t r : {fast::set_attrs<32>(), fast::set_attrs<64>(),
+                          cudaFuncSetAttribute(fast::k_gs_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * fast::TR * 32 * 4 + 64),
+                          cudaFuncSetAttribute(fast::k_gs_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * fast::TR * 64 * 4 + 64)})
         if (r != cudaSuccess) e = r;
     return e;
 }
@@ -1098,6 +1154,22 @@ cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_o
     if (a.w <= 32) return fast::launch_w<32>(kind, a, s, grid_out);
     if (a.w <= 64) return fast::launch_w<64>(kind, a, s, grid_out);
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gs_tma(const GsArgs& a, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    if (a.k < 1 || a.k > 16 || a.w > 64 || a.nplanes < 1 || a.nplanes > kMaxDst) return cudaErrorInvalidValue;
+    const int tiles = (a.n + fast::TR - 1) / fast::TR;
+    const int cap = tile::sm_count_host() * 3;
+    const int grid = tiles < cap ? tiles : cap;
+    if (a.w <= 32) {
+        constexpr size_t bytes = 2 * fast::TR * 32 * 4 + 64;
+        fast::k_gs_tma<32><<<grid, fast::TR, bytes, s>>>(a);
+    } else {
+        constexpr size_t bytes = 2 * fast::TR * 64 * 4 + 64;
+        fast::k_gs_tma<64><<<grid, fast::TR, bytes, s>>>(a);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_hub_segs(bool sparse, const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub,

@@ -127,7 +127,13 @@ struct GsArgs {
     const float* planes[kMaxDst] = {};
     int nplanes = 1;
     std::uint8_t* rec = nullptr;
+    CUtensorMap maps[kMaxDst];  // launch_gs_tma: TMA maps of the planes
 };
+
+// GS top-k of (a left-to-right sum of) planes, thread per row over TMA-loaded
+// tiles (fast.cu; w ≤ 64, k ≤ 16)
+cudaError_t launch_gs_tma(const GsArgs& a, cudaStream_t s);
+
 
 // Host launchers (kernels.cu). All enqueue on `s` and return cudaError_t.
 cudaError_t launch_tile(const TileArgs& a, cudaStream_t s, int* grid_out);  // grid = SMs × occupancy
