@@ -67,13 +67,26 @@ __global__ void __launch_bounds__(kThreads) k_gs(GsArgs a) {
 }
 
 // Fixed-order reduction of per-CTA partials (double) into a float gradient.
-__global__ void k_reduce_parts(const double* __restrict__ part, int nparts, int stride, int len, float* __restrict__ out, int accumulate) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= len) return;
+// 32 outputs per block, each summed by 8 warps over contiguous partial
+// ranges in fixed order, the 8 range sums then added in order: deterministic,
+// coalesced across the 32 outputs, and 8× the parallelism of a thread per output.
+__global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__ part, int nparts, int stride, int len, float* __restrict__ out,
+                                                      int accumulate) {
+    __shared__ double red[8][32];
+    const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + lane;
+    const int per = (nparts + 7) / 8, p0 = c * per, p1 = min(nparts, p0 + per);
     double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[static_cast<size_t>(p) * stride + i];
-    if (accumulate) s += static_cast<double>(out[i]);
-    out[i] = static_cast<float>(s);
+    if (i < len)
+        for (int p = p0; p < p1; ++p) s += part[static_cast<size_t>(p) * stride + i];
+    red[c][lane] = s;
+    __syncthreads();
+    if (c == 0 && i < len) {
+        double t = red[0][lane];
+        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        if (accumulate) t += static_cast<double>(out[i]);
+        out[i] = static_cast<float>(t);
+    }
 }
 
 // Single-CTA fixed-order sum of n doubles (loss partials), scaled.
@@ -333,7 +346,7 @@ cudaError_t launch_gs(const GsArgs& a, cudaStream_t s) {
 
 cudaError_t launch_reduce_parts(const double* part, int nparts, int stride, int len, float* out, int accumulate, cudaStream_t s) {
     if (len <= 0) return cudaSuccess;
-    k_reduce_parts<<<blocks_for(len, 256), 256, 0, s>>>(part, nparts, stride, len, out, accumulate);
+    k_reduce_parts<<<blocks_for(len, 32), 256, 0, s>>>(part, nparts, stride, len, out, accumulate);
     return cudaGetLastError();
 }
 
