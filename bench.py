@@ -132,6 +132,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def load_traffic(cfg_name):
+    """Measured DRAM bytes per launch (ncu --set full, committed under profiles/) for the c3 kernel classes."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if cfg_name != "c3" or not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f)
+
+
 def build_inputs(cfg_name, rank):
     from paper_2603_27156_b200 import synth
     gname = CONFIGS[cfg_name][0]
@@ -289,11 +298,13 @@ def run_ours(args):
         top = max(share, key=share.get)
         kv = kernels[top]
         achieved = kv["bytes"] / (kv["ms"] * 1e-3) / 1e9
+        traffic = load_traffic(args.config)
         roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None, "peak_source": peak_src, "ms_per_launch": kv["ms"],
+                "traffic": traffic.get(top), "traffic_source": traffic.get("source"), "peak_source": peak_src, "ms_per_launch": kv["ms"],
                 "share_of_step": share[top] / ms_step,
                 "algorithmic_bytes_per_launch": kv["bytes"]}
         for n, v in kernels.items():
+            v["dram_traffic_bytes"] = traffic.get(n)
             v["achieved_gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
             v["frac_hbm"] = v["achieved_gbs"] / hbm_peak
             v["share_of_step"] = share[n] / ms_step
