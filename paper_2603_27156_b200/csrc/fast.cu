@@ -685,30 +685,67 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             tile::tc_fence_after();
             dw_pending = false;
         }
-        // ---- Y = Âᵀ·x_in: this thread's column half of row t
-        float rf = 0.f;
-        if (valid) {
-            const int e0 = __ldg(a.dir.ptr + row), ne = __ldg(a.dir.ptr + row + 1) - e0;
-            rf = __ldg(a.dir.out_f + row);
-            if (ne > kSegF) {
-                const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
+        // ---- Y = Âᵀ·x_in, gathered cooperatively: an 8-lane group per row, lane
+        // q owning the 16 B column chunks q and q + 8 (W = 64), so every
+        // neighbour-row load is four whole 128 B lines per warp instruction
+        // (not 32 scattered sectors); up to 8 edges of loads in flight per lane.
+        {
+            constexpr int NCH = W / 32;  // 16 B chunks per lane: columns 4q (+32)
+            const int grp = tid >> 3, q = tid & 7;
+#pragma unroll 1
+            for (int pass = 0; pass < TR / 32; ++pass) {
+                const int r = pass * 32 + grp, rw = row0 + r;
+                float4 acc[NCH];
 #pragma unroll
-                for (int c = 0; c < HW; c += 4)
-                    *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c)) = c_lo + c < a.ld ? dev::ld4(zh + c_lo + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-                agg_dense_half<W>(a, e0, ne, Zs, t, hf);
+                for (int h = 0; h < NCH; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+                // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
+                float rfr = 0.f;
+                int e0 = 0, ne = 0;
+                if (rw < a.n) {
+                    e0 = __ldg(a.dir.ptr + rw);
+                    ne = __ldg(a.dir.ptr + rw + 1) - e0;
+                    rfr = __ldg(a.dir.out_f + rw);
+                }
+                const bool hub = ne > kSegF;
+                if (hub) {
+                    const float* zh = a.Zh + static_cast<size_t>(rw) * a.ld;
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h)
+                        if (32 * h + 4 * q < a.ld) acc[h] = dev::ld4(zh + 32 * h + 4 * q);
+                }
+                const int nr = hub ? 0 : ne;  // regular-row edges (0 for hubs / padding rows)
+                const bool unit = a.dir.unit_edge != 0;
+                const int myc = q < nr ? __ldg(a.dir.idx + e0 + q) : 0;
+                const float mysc = (!unit && q < nr) ? __ldg(a.dir.edge_f + myc) : 1.f;
+                float4 x[kSegF][NCH];
+#pragma unroll
+                for (int u = 0; u < kSegF; ++u) {
+                    const int c = __shfl_sync(0xffffffffu, myc, u, 8);
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h)
+                        x[u][h] = (u < nr && 32 * h + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 32 * h + 4 * q)
+                                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kSegF; ++u) {
+                    const float sc = __shfl_sync(0xffffffffu, mysc, u, 8);
+                    if (u < nr) {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h) {
+                            acc[h].x = __fadd_rn(acc[h].x, __fmul_rn(sc, x[u][h].x));
+                            acc[h].y = __fadd_rn(acc[h].y, __fmul_rn(sc, x[u][h].y));
+                            acc[h].z = __fadd_rn(acc[h].z, __fmul_rn(sc, x[u][h].z));
+                            acc[h].w = __fadd_rn(acc[h].w, __fmul_rn(sc, x[u][h].w));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {  // Â scale; Y in K-major (MMA A) and BASE32B (dW B)
+                    const float4 v = make_float4(__fmul_rn(rfr, acc[h].x), __fmul_rn(rfr, acc[h].y), __fmul_rn(rfr, acc[h].z), __fmul_rn(rfr, acc[h].w));
+                    *reinterpret_cast<float4*>(Zs + zo(r, 32 * h + 4 * q)) = v;
+                    *reinterpret_cast<float4*>(Y2 + zb(r, 32 * h + 4 * q)) = v;
+                }
             }
-        } else {
-#pragma unroll
-            for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int c = 0; c < HW; c += 4) {  // Â scale; Y2 = Y in BASE32B for dW
-            float4* p = reinterpret_cast<float4*>(Zs + zo(t, c_lo + c));
-            float4 v = *p;
-            v.x = __fmul_rn(rf, v.x); v.y = __fmul_rn(rf, v.y); v.z = __fmul_rn(rf, v.z); v.w = __fmul_rn(rf, v.w);
-            *p = v;
-            *reinterpret_cast<float4*>(Y2 + zb(t, c_lo + c)) = v;
         }
         tile::fence_proxy_async();
         __syncthreads();
