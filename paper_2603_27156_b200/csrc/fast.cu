@@ -250,97 +250,123 @@ __device__ __forceinline__ void agg_dense_row(const FastArgs& a, int e0, int ne,
 }
 
 // GS top-k of a row held in a swizzled smem tile → CBSR record.
-// Same selection as dev::gs_select_row: k-th largest magnitude key T via a
-// bitonic top-G tree, then columns ascending, ties at T lowest column first.
-template <int W, int G>
-__device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
+// Selection: the k largest magnitudes, ties at the threshold T (the k-th
+// largest key) taken lowest column first, columns ascending — the oracle's
+// gs_topk. T comes from a top-G tree over the W keys: each G-key group sorted
+// by Batcher's odd-even merge network (63 compare-exchanges for G = 16), groups
+// merged pairwise by a half-cleaner + bitonic merge; when k == G the last level
+// needs only the half-cleaner and a min (T = the smallest of the top G).
+// Selection mask: keys ≥ T; only rows with extra ties at T take the slow path.
+// Batcher odd-even merge sort, n = 16: 63 compare-exchanges (i, j), max → i
+constexpr int kOem16N = 63;
+__host__ __device__ constexpr int oem16(int i) {
+    constexpr int p[126] = {0, 1, 2, 3, 0, 2, 1, 3, 1, 2, 4, 5, 6, 7, 4, 6, 5, 7, 5, 6, 0, 4, 2, 6, 2, 4, 1, 5, 3, 7, 3, 5,
+                                   1, 2, 3, 4, 5, 6, 8, 9, 10, 11, 8, 10, 9, 11, 9, 10, 12, 13, 14, 15, 12, 14, 13, 15, 13, 14, 8, 12,
+                                   10, 14, 10, 12, 9, 13, 11, 15, 11, 13, 9, 10, 11, 12, 13, 14, 0, 8, 4, 12, 4, 8, 2, 10, 6, 14, 6, 10,
+                                   2, 4, 6, 8, 10, 12, 1, 9, 5, 13, 5, 9, 3, 11, 7, 15, 7, 11, 3, 5, 7, 9, 11, 13, 1, 2, 3, 4, 5, 6, 7,
+                                   8, 9, 10, 11, 12, 13, 14};
+    return p[i];
+}
+
+template <int W, bool FULLW>
+__device__ __forceinline__ uint32_t gs_key(float v, int col, int w) {
+    // |x| bit pattern; +1 only when padding columns (key 0) must rank below real zeros
+    if (FULLW) return __float_as_uint(v) & 0x7fffffffu;
+    return col < w ? (__float_as_uint(v) & 0x7fffffffu) + 1u : 0u;
+}
+
+template <int W, bool FULLW>
+__device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
+    constexpr int G = 16;
+    constexpr int LW = W == 64 ? 6 : 5;
+    static_assert((1 << LW) == W, "W must be 32 or 64");
     uint32_t s[W];
 #pragma unroll
     for (int c = 0; c < W; c += 4) {
         const float4 v = *reinterpret_cast<const float4*>(Ts + zo(r, c));
-        s[c] = c < w ? dev::mag_key(v.x) : 0u;
-        s[c + 1] = c + 1 < w ? dev::mag_key(v.y) : 0u;
-        s[c + 2] = c + 2 < w ? dev::mag_key(v.z) : 0u;
-        s[c + 3] = c + 3 < w ? dev::mag_key(v.w) : 0u;
+        s[c] = gs_key<W, FULLW>(v.x, c, w);
+        s[c + 1] = gs_key<W, FULLW>(v.y, c + 1, w);
+        s[c + 2] = gs_key<W, FULLW>(v.z, c + 2, w);
+        s[c + 3] = gs_key<W, FULLW>(v.w, c + 3, w);
     }
-    // bitonic sort of every G-key group (descending), all indices compile-time
-    constexpr int LG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
-    static_assert((1 << LG) == G, "G must be a power of two <= 16");
-    constexpr int LW = W == 128 ? 7 : (W == 64 ? 6 : (W == 32 ? 5 : 0));
-    static_assert((1 << LW) == W, "W must be 32 or 64");
 #pragma unroll
-    for (int ls = 1; ls <= LG; ++ls) {
-        const int size = 1 << ls;
+    for (int g = 0; g < W; g += G)
 #pragma unroll
-        for (int lt = ls - 1; lt >= 0; --lt) {
+        for (int i = 0; i < kOem16N; ++i) {
+            const int x = g + oem16(2 * i), y = g + oem16(2 * i + 1);
+            const uint32_t hi = max(s[x], s[y]), lo = min(s[x], s[y]);
+            s[x] = hi;
+            s[y] = lo;
+        }
+    auto merge = [&](int ga, int gb, bool sort) {  // top-G of sorted groups ga ∪ gb → ga
+#pragma unroll
+        for (int i = 0; i < G; ++i) s[ga + i] = max(s[ga + i], s[gb + G - 1 - i]);
+        if (!sort) return;
+#pragma unroll
+        for (int lt = 3; lt >= 0; --lt) {
             const int stride = 1 << lt;
 #pragma unroll
-            for (int i = 0; i < W; ++i) {
+            for (int i = 0; i < G; ++i) {
                 const int j = i ^ stride;
                 if (j > i) {
-                    const uint32_t x = s[i], y = s[j];
-                    const uint32_t hi = max(x, y), lo = min(x, y);
-                    if (((i % G) & size) == 0) { s[i] = hi; s[j] = lo; }
-                    else { s[i] = lo; s[j] = hi; }
+                    const uint32_t x = s[ga + i], y = s[ga + j];
+                    s[ga + i] = max(x, y);
+                    s[ga + j] = min(x, y);
                 }
             }
         }
-    }
-    // merge tree: top-G of groups (g, g + span) → group g, sorted
+    };
 #pragma unroll
-    for (int lsp = LG; lsp < LW; ++lsp) {
+    for (int lsp = 4; lsp < LW - 1; ++lsp) {  // all but the last level keep the groups sorted
         const int span = 1 << lsp;
 #pragma unroll
-        for (int g = 0; g < W; g += 2 * span) {
-#pragma unroll
-            for (int i = 0; i < G; ++i) s[g + i] = max(s[g + i], s[g + span + G - 1 - i]);
-#pragma unroll
-            for (int lt = LG - 1; lt >= 0; --lt) {
-                const int stride = 1 << lt;
-#pragma unroll
-                for (int i = 0; i < G; ++i) {
-                    const int j = i ^ stride;
-                    if (j > i) {
-                        const uint32_t x = s[g + i], y = s[g + j];
-                        s[g + i] = max(x, y);
-                        s[g + j] = min(x, y);
-                    }
-                }
-            }
-        }
+        for (int g = 0; g < W; g += 2 * span) merge(g, g + span, true);
     }
-    // T = s[k-1] = min of the first k (descending); a select chain here would
-    // be folded into a dynamically indexed (local-memory) load
     uint32_t T = 0xffffffffu;
+    if (k == G) {  // last level: the top G as a set; T is its minimum
+        merge(0, W / 2, false);
 #pragma unroll
-    for (int i = 0; i < G; ++i) T = min(T, i < k ? s[i] : 0xffffffffu);
-    int gt = 0;
+        for (int i = 0; i < G; ++i) T = min(T, s[i]);
+    } else {
+        merge(0, W / 2, true);
 #pragma unroll
-    for (int i = 0; i < G; ++i) gt += s[i] > T;
-    int take = k - gt;
-    // selection as a column bitmask: every key > T, plus the first `take` keys == T
+        for (int i = 0; i < G; ++i) T = min(T, i < k ? s[i] : 0xffffffffu);
+    }
+    // selection mask: every key ≥ T, unless extra ties at T must be cut
     constexpr int NWD = W / 32;
-    uint32_t gm[NWD], em[NWD];
+    uint32_t ge[NWD];
 #pragma unroll
-    for (int q = 0; q < NWD; ++q) { gm[q] = 0u; em[q] = 0u; }
+    for (int q = 0; q < NWD; ++q) ge[q] = 0u;
 #pragma unroll
     for (int c = 0; c < W; c += 4) {
         const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
         const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int col = c + q;
-            const uint32_t key = col < w ? dev::mag_key(vv[q]) : 0u;
-            gm[col >> 5] |= static_cast<uint32_t>(key > T) << (col & 31);
-            em[col >> 5] |= static_cast<uint32_t>(key == T) << (col & 31);
-        }
+        for (int q = 0; q < 4; ++q) ge[(c + q) >> 5] |= static_cast<uint32_t>(gs_key<W, FULLW>(vv[q], c + q, w) >= T) << ((c + q) & 31);
     }
+    int cnt = 0;
 #pragma unroll
-    for (int q = 0; q < NWD; ++q) {  // ties at T: lowest columns first
-        while (take > 0 && em[q]) {
-            gm[q] |= em[q] & (0u - em[q]);
-            em[q] &= em[q] - 1u;
-            --take;
+    for (int q = 0; q < NWD; ++q) cnt += __popc(ge[q]);
+    if (cnt != k) {  // ties at T beyond k: keep keys > T, then the lowest-column ties
+        uint32_t gt[NWD];
+#pragma unroll
+        for (int q = 0; q < NWD; ++q) gt[q] = 0u;
+        for (int c = 0; c < W; ++c) {
+            const float v = Ts[zo(r, c)];
+            gt[c >> 5] |= static_cast<uint32_t>(gs_key<W, FULLW>(v, c, w) > T) << (c & 31);
+        }
+        int take = k;
+#pragma unroll
+        for (int q = 0; q < NWD; ++q) take -= __popc(gt[q]);
+#pragma unroll
+        for (int q = 0; q < NWD; ++q) {
+            uint32_t eq = ge[q] & ~gt[q];
+            while (take > 0 && eq) {
+                gt[q] |= eq & (0u - eq);
+                eq &= eq - 1u;
+                --take;
+            }
+            ge[q] = gt[q];
         }
     }
     // emit the k selected columns in ascending order with compile-time slots
@@ -348,7 +374,7 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
     // with 128-bit stores (layout: 16 index bytes, then k values, 16 B padded)
     uint32_t iw[4] = {0u, 0u, 0u, 0u};
     float rv[16];
-    uint32_t m0 = gm[0], m1 = NWD > 1 ? gm[NWD - 1] : 0u;
+    uint32_t m0 = ge[0], m1 = NWD > 1 ? ge[NWD - 1] : 0u;
 #pragma unroll
     for (int slot = 0; slot < 16; ++slot) {
         rv[slot] = 0.f;
@@ -366,6 +392,13 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         if (q < nv4) reinterpret_cast<float4*>(rec_out + 16)[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+}
+
+template <int W, int G>
+__device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
+    static_assert(G == 16, "top-16 tree (k ≤ 16)");
+    if (w == W) gs_row_impl<W, true>(Ts, r, w, k, rec_out);
+    else gs_row_impl<W, false>(Ts, r, w, k, rec_out);
 }
 
 template <int W, int KIND, int KS>
