@@ -724,32 +724,51 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
         // (not 32 scattered sectors); up to 8 edges of loads in flight per lane.
         {
             constexpr int NCH = W / 32;  // 16 B chunks per lane: columns 4q (+32)
+            constexpr int NP = TR / 32;  // passes of 32 rows
             const int grp = tid >> 3, q = tid & 7;
+            const bool unit = a.dir.unit_edge != 0;
+            // the CSR metadata of all passes first (row range → neighbour ids →
+            // edge scales): three dependent latencies per tile, not per pass
+            int e0v[NP], nrv[NP];
+            float rfv[NP];
+            bool hubv[NP];
+#pragma unroll
+            for (int ps = 0; ps < NP; ++ps) {
+                const int rw = row0 + ps * 32 + grp;
+                e0v[ps] = 0; nrv[ps] = 0; rfv[ps] = 0.f;
+                if (rw < a.n) {
+                    e0v[ps] = __ldg(a.dir.ptr + rw);
+                    nrv[ps] = __ldg(a.dir.ptr + rw + 1) - e0v[ps];
+                    rfv[ps] = __ldg(a.dir.out_f + rw);
+                }
+                hubv[ps] = nrv[ps] > kSegF;
+                if (hubv[ps]) nrv[ps] = 0;
+            }
+            int mycv[NP];
+#pragma unroll
+            for (int ps = 0; ps < NP; ++ps) mycv[ps] = q < nrv[ps] ? __ldg(a.dir.idx + e0v[ps] + q) : 0;
+            float myscv[NP];
+#pragma unroll
+            for (int ps = 0; ps < NP; ++ps) myscv[ps] = (!unit && q < nrv[ps]) ? __ldg(a.dir.edge_f + mycv[ps]) : 1.f;
 #pragma unroll 1
-            for (int pass = 0; pass < TR / 32; ++pass) {
+            for (int pass = 0; pass < NP; ++pass) {
                 const int r = pass * 32 + grp, rw = row0 + r;
+                int nr = 0, myc = 0;
+                float mysc = 1.f, rfr = 0.f;
+                bool hub = false;
+#pragma unroll
+                for (int ps = 0; ps < NP; ++ps)
+                    if (ps == pass) { nr = nrv[ps]; myc = mycv[ps]; mysc = myscv[ps]; rfr = rfv[ps]; hub = hubv[ps]; }
                 float4 acc[NCH];
 #pragma unroll
                 for (int h = 0; h < NCH; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-                // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
-                float rfr = 0.f;
-                int e0 = 0, ne = 0;
-                if (rw < a.n) {
-                    e0 = __ldg(a.dir.ptr + rw);
-                    ne = __ldg(a.dir.ptr + rw + 1) - e0;
-                    rfr = __ldg(a.dir.out_f + rw);
-                }
-                const bool hub = ne > kSegF;
                 if (hub) {
                     const float* zh = a.Zh + static_cast<size_t>(rw) * a.ld;
 #pragma unroll
                     for (int h = 0; h < NCH; ++h)
                         if (32 * h + 4 * q < a.ld) acc[h] = dev::ld4(zh + 32 * h + 4 * q);
                 }
-                const int nr = hub ? 0 : ne;  // regular-row edges (0 for hubs / padding rows)
-                const bool unit = a.dir.unit_edge != 0;
-                const int myc = q < nr ? __ldg(a.dir.idx + e0 + q) : 0;
-                const float mysc = (!unit && q < nr) ? __ldg(a.dir.edge_f + myc) : 1.f;
+                // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
                 float4 x[kSegF][NCH];
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
