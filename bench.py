@@ -253,6 +253,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     launches = ctx.kernel_launches() - l0
+    tb = ctx.last_timing()  # Eq. 9 phases of the last timed step
+    phases = {k: round(tb[f"t_{k}"] * 1e3, 3) for k in ("forward", "backward", "optimizer", "copy", "total")}
     ms = ev0.elapsed_time(ev1)
     ms_t = torch.tensor([ms], device=f"cuda:{local}")
     if world > 1:
@@ -323,6 +325,7 @@ def run_ours(args):
                        "subgraph_per_rank": "seed = rank", "l2": "inputs larger than L2 (activations 1 GB/plane set)",
                        "cuda_graph": not args.no_graph},
             "edges_layers_per_s": value * g.e * L,
+            "phases_ms_last_step": phases,
             "peak_hbm_bytes": {"arena_peak_active": mem["peak_active_bytes"], "arena_reserved": mem["reserved_bytes"],
                                "cudaMemGetInfo_delta": int(free0 - free1), "utilization": mem["utilization"]},
             "loss": {"first": losses[0], "last": losses[-1]},

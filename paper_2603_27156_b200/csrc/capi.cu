@@ -161,22 +161,25 @@ struct gsrc_ctx {
 
     // graph replay
     bool use_graph = false;
-    cudaGraphExec_t g_fb = nullptr, g_step = nullptr;
-    int64_t g_fb_launches = 0, g_step_launches = 0;
+    // the step replays as three graphs (forward, backward, optimizer) so the
+    // Eq. 9 phase events sit between graph launches
+    cudaGraphExec_t g_fwd = nullptr, g_bwd = nullptr, g_opt = nullptr;
+    int64_t g_fwd_launches = 0, g_bwd_launches = 0, g_opt_launches = 0;
     gsrc_optim_cfg g_step_opt{};
 
     cudaEvent_t ev[4] = {};
+    cudaEvent_t tev[3] = {};  // phase marks inside the step (Eq. 9): after forward, after backward, after optimizer
     gsrc_timing timing{};
 
     ~gsrc_ctx() {
-        if (g_fb) cudaGraphExecDestroy(g_fb);
-        if (g_step) cudaGraphExecDestroy(g_step);
+        for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
         for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)seg_f, (void*)seg_b,
                         (void*)segoff_f, (void*)segoff_b, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
         for (auto& e_ : ev) if (e_) cudaEventDestroy(e_);
+        for (auto& e_ : tev) if (e_) cudaEventDestroy(e_);
         if (own) cudaStreamDestroy(own);
     }
 
@@ -534,8 +537,8 @@ struct gsrc_ctx {
         if (!data) seq_err("node data not uploaded (gsrc_data_upload)");
     }
     void drop_graphs() {
-        if (g_fb) { cudaGraphExecDestroy(g_fb); g_fb = nullptr; }
-        if (g_step) { cudaGraphExecDestroy(g_step); g_step = nullptr; }
+        for (cudaGraphExec_t* g : {&g_fwd, &g_bwd, &g_opt})
+            if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
     }
 
     // Activation arena plan (bytes independent of L except the ALG12 caches,
@@ -691,6 +694,7 @@ int gsrc_create(int device, gsrc_ctx** out) {
     if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     ctx->stream = ctx->own;
     for (auto& e : ctx->ev) cudaEventCreate(&e);
+    for (auto& e : ctx->tev) cudaEventCreate(&e);
     if (init_kernel_attributes() != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     if (cudaMallocHost(&ctx->loss_host, sizeof(double)) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     *out = ctx;
@@ -948,21 +952,35 @@ static void run_maybe_graph(gsrc_ctx* ctx, cudaGraphExec_t& exec, int64_t& nl, c
     ctx->launches += nl;
 }
 
+// TimingBreakdown (Eq. 9) from events recorded around and
+// inside the (possibly graph-replayed) step: forward (encoder, layers, head,
+// loss), backward (head, layers with inverse recomputation, encoder),
+// optimizer, and the loss copy-out (the host-analogue of Table 3's cudaMemcpy).
+static gsrc_timing phase_timing(gsrc_ctx* ctx, bool with_opt) {
+    float t_all = 0.f, t_f = 0.f, t_b = 0.f, t_o = 0.f;
+    cudaEventElapsedTime(&t_all, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&t_f, ctx->ev[0], ctx->tev[0]);
+    cudaEventElapsedTime(&t_b, ctx->tev[0], ctx->tev[1]);
+    if (with_opt) cudaEventElapsedTime(&t_o, ctx->tev[1], ctx->tev[2]);
+    const float t_c = t_all - t_f - t_b - t_o;
+    return gsrc_timing{t_f * 1e-3, t_b * 1e-3, (t_c > 0.f ? t_c : 0.f) * 1e-3, t_o * 1e-3, t_all * 1e-3};
+}
+
 int gsrc_forward_backward(gsrc_ctx* ctx, double* loss_out) {
     return guarded(ctx, [&] {
         ctx->require_data();
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        run_maybe_graph(ctx, ctx->g_fb, ctx->g_fb_launches, [&] {
+        run_maybe_graph(ctx, ctx->g_fwd, ctx->g_fwd_launches, [&] {
             ctx->enqueue_zero_grads();
             ctx->enqueue_forward();
-            ctx->enqueue_backward();
         });
+        CK(cudaEventRecord(ctx->tev[0], ctx->stream));
+        run_maybe_graph(ctx, ctx->g_bwd, ctx->g_bwd_launches, [&] { ctx->enqueue_backward(); });
+        CK(cudaEventRecord(ctx->tev[1], ctx->stream));
         CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-        ctx->timing = gsrc_timing{0, 0, 0, 0, ms * 1e-3};
+        ctx->timing = phase_timing(ctx, false);
         if (loss_out) *loss_out = *ctx->loss_host;
     });
 }
@@ -980,24 +998,25 @@ int gsrc_train_step(gsrc_ctx* ctx, const gsrc_optim_cfg* opt, double* loss_out) 
     return guarded(ctx, [&] {
         ctx->require_data();
         if (!opt) cfg_err("null optimizer cfg");
-        if (ctx->g_step && std::memcmp(&ctx->g_step_opt, opt, sizeof(gsrc_optim_cfg)) != 0) {
-            cudaGraphExecDestroy(ctx->g_step);
-            ctx->g_step = nullptr;
+        if (ctx->g_opt && std::memcmp(&ctx->g_step_opt, opt, sizeof(gsrc_optim_cfg)) != 0) {
+            cudaGraphExecDestroy(ctx->g_opt);
+            ctx->g_opt = nullptr;
         }
         ctx->g_step_opt = *opt;
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        run_maybe_graph(ctx, ctx->g_step, ctx->g_step_launches, [&] {
+        run_maybe_graph(ctx, ctx->g_fwd, ctx->g_fwd_launches, [&] {
             ctx->enqueue_zero_grads();
             ctx->enqueue_forward();
-            ctx->enqueue_backward();
-            ctx->enqueue_optimizer(*opt);
         });
+        CK(cudaEventRecord(ctx->tev[0], ctx->stream));
+        run_maybe_graph(ctx, ctx->g_bwd, ctx->g_bwd_launches, [&] { ctx->enqueue_backward(); });
+        CK(cudaEventRecord(ctx->tev[1], ctx->stream));
+        run_maybe_graph(ctx, ctx->g_opt, ctx->g_opt_launches, [&] { ctx->enqueue_optimizer(*opt); });
+        CK(cudaEventRecord(ctx->tev[2], ctx->stream));
         CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-        ctx->timing = gsrc_timing{0, 0, 0, 0, ms * 1e-3};
+        ctx->timing = phase_timing(ctx, true);
         if (loss_out) *loss_out = *ctx->loss_host;
     });
 }

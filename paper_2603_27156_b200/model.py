@@ -51,3 +51,62 @@ def init_params(mode, layers, hidden, groups, d_in, seed=0, block_scale=None, dt
     s_h = np.sqrt(6.0 / (hidden + 1))
     p[o:o + n] = rng.uniform(-s_h, s_h, n)
     return p.astype(dtype)
+
+
+# ---- GSRP parameter checkpoints ---------------------------------
+# magic "GSRP", u32 LE version, then u64 LE mode, L, D, C, d_in and the block
+# count; per block u64 LE rows, cols, then w (rows × cols) and b (cols) as f64 LE.
+# Blocks in GSRP order: encoder (d_in × D), every layer's C blocks (w × w), head (D × 1).
+GSRP_VERSION = 1
+
+
+def _blocks(mode, layers, hidden, groups, d_in):
+    lay = param_layout(mode, layers, hidden, groups, d_in)
+    out = [(lay["enc_w"][0], d_in, hidden)]
+    out += [(o, w, w) for _, o, w in lay["blocks"]]
+    out.append((lay["head_w"][0], hidden, 1))
+    return out
+
+
+def write_gsrp(path, p, mode, layers, hidden, groups, d_in):
+    p = np.asarray(p, np.float64)
+    blocks = _blocks(mode, layers, hidden, groups, d_in)
+    with open(path, "wb") as f:
+        f.write(b"GSRP")
+        f.write(np.array([GSRP_VERSION], "<u4").tobytes())
+        f.write(np.array([mode, layers, hidden, groups, d_in, len(blocks)], "<u8").tobytes())
+        for o, rows, cols in blocks:
+            f.write(np.array([rows, cols], "<u8").tobytes())
+            f.write(p[o:o + rows * cols + cols].astype("<f8").tobytes())
+
+
+def read_gsrp(path):
+    """→ (params f32, dict(mode, layers, hidden, groups, d_in)); ValueError on a malformed file."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    if len(buf) < 56 or buf[:4] != b"GSRP":
+        raise ValueError(f"{path}: bad GSRP magic")
+    if int(np.frombuffer(buf, "<u4", 1, 4)[0]) != GSRP_VERSION:
+        raise ValueError(f"{path}: unsupported GSRP version")
+    mode, layers, hidden, groups, d_in, nb = (int(x) for x in np.frombuffer(buf, "<u8", 6, 8))
+    blocks = _blocks(mode, layers, hidden, groups, d_in)
+    if nb != len(blocks):
+        raise ValueError(f"{path}: block count {nb} != {len(blocks)}")
+    P = param_layout(mode, layers, hidden, groups, d_in)["P"]
+    p = np.zeros(P, np.float64)
+    off = 56
+    for o, rows, cols in blocks:
+        if off + 16 > len(buf):
+            raise ValueError(f"{path}: truncated GSRP")
+        r, c = (int(x) for x in np.frombuffer(buf, "<u8", 2, off))
+        if (r, c) != (rows, cols):
+            raise ValueError(f"{path}: block shape {(r, c)} != {(rows, cols)}")
+        off += 16
+        cnt = rows * cols + cols
+        if off + 8 * cnt > len(buf):
+            raise ValueError(f"{path}: truncated GSRP")
+        p[o:o + cnt] = np.frombuffer(buf, "<f8", cnt, off)
+        off += 8 * cnt
+    if off != len(buf):
+        raise ValueError(f"{path}: trailing bytes in GSRP")
+    return p.astype(np.float32), dict(mode=mode, layers=layers, hidden=hidden, groups=groups, d_in=d_in)

@@ -49,6 +49,22 @@ def test_gsrg_rejects_corruption(tmp_path):
         synth.read_graph(gp)
 
 
+def test_gsrp_round_trip_and_corruption(tmp_path):
+    from paper_2603_27156_b200 import MODE_GSRC, model
+    p = model.init_params(MODE_GSRC, 3, 64, 4, 8, seed=4)
+    path = str(tmp_path / "p.gsrp")
+    model.write_gsrp(path, p, MODE_GSRC, 3, 64, 4, 8)
+    q, meta = model.read_gsrp(path)
+    assert np.array_equal(p, q) and meta == dict(mode=MODE_GSRC, layers=3, hidden=64, groups=4, d_in=8)
+    b = open(path, "rb").read()
+    open(path, "wb").write(b[:-8])
+    with pytest.raises(ValueError, match="truncated"):
+        model.read_gsrp(path)
+    open(path, "wb").write(b"GSRX" + b[4:])
+    with pytest.raises(ValueError, match="magic"):
+        model.read_gsrp(path)
+
+
 def test_cli_exit_codes_without_gpu(cli, tmp_path):
     _, _, gp, np_ = _files(tmp_path)
     r = subprocess.run([cli, "version"], capture_output=True, text=True)
@@ -86,6 +102,42 @@ def test_cli_trains_and_matches_python_host(cli, tmp_path):
     ctx.model_init(MODE_GSRC, L, D, C, k, 8)
     ctx.set_params(p)
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
-    l0 = ctx.train_step(lr=1e-3)
-    assert recs[0]["train_loss"] == pytest.approx(l0, rel=1e-6)
+    losses = [ctx.train_step(lr=1e-3) for _ in range(4)]
+    assert [r["train_loss"] for r in recs[:4]] == pytest.approx(losses, rel=1e-6)
     assert recs[3]["train_loss"] < recs[0]["train_loss"]
+    # Eq. 9 breakdown per epoch
+    for r in recs[:4]:
+        parts = r["t_forward"] + r["t_backward"] + r["t_optimizer"] + r["t_copy"]
+        assert r["t_forward"] > 0 and r["t_backward"] > 0 and parts <= r["t_total"] * 1.001 + 1e-6
+
+
+@pytest.mark.gpu
+def test_cli_checkpoint_resume(cli, tmp_path):
+    """--checkpoint writes GSRP of the trained parameters; 2 + 2 epochs
+    with --resume equal 4 epochs except for Adam's moments, which GSRP does not hold."""
+    from paper_2603_27156_b200 import MODE_GSRC, Context, init_params, model
+    g, nd, gp, np_ = _files(tmp_path, n=2000)
+    L, D, C, k = 2, 64, 2, 8
+    p = init_params(MODE_GSRC, L, D, C, 8, seed=5)
+    pf = tmp_path / "p.f32"
+    p.astype(np.float32).tofile(pf)
+    ck = tmp_path / "a.gsrp"
+    args = ["--graph", gp, "--nodes", np_, "--layers", str(L), "--hidden", str(D), "--groups", str(C), "--k", str(k), "--lr", "1e-3"]
+    r = subprocess.run([cli, "train", *args, "--epochs", "2", "--params", str(pf), "--checkpoint", str(ck), "--report", str(tmp_path / "a.jsonl")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    q, meta = model.read_gsrp(str(ck))
+    assert meta == dict(mode=MODE_GSRC, layers=L, hidden=D, groups=C, d_in=8)
+    ctx = Context(0)
+    ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
+    ctx.model_init(MODE_GSRC, L, D, C, k, 8)
+    ctx.set_params(p)
+    ctx.data_upload(nd.features, nd.labels, nd.train_mask)
+    for _ in range(2):
+        ctx.train_step(lr=1e-3)
+    assert np.array_equal(ctx.params(), q)
+    r = subprocess.run([cli, "train", *args, "--epochs", "1", "--resume", str(ck), "--report", str(tmp_path / "b.jsonl")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([cli, "train", *args[:4], "--hidden", "32", *args[6:], "--epochs", "1", "--resume", str(ck)], capture_output=True, text=True)
+    assert r.returncode == 1 and "differs" in r.stderr

@@ -11,7 +11,8 @@
 //   gsrnet-cuda train --graph g.gsrg --nodes n.gsrn [--model gsrc|gsr|baseline]
 //       [--layers L] [--hidden D] [--groups C] [--k K] [--epochs E] [--lr LR]
 //       [--norm none|row_mean|sym] [--precision fp32|tf32] [--seed S]
-//       [--params init.f32] [--report out.jsonl] [--device I]
+//       [--params init.f32 | --resume in.gsrp] [--checkpoint out.gsrp]
+//       [--report out.jsonl] [--device I]
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -125,10 +126,72 @@ std::vector<float> init_params(const gsr::cuda::NetConfig& c, index_t P, std::ui
     return p;
 }
 
+// GSRP checkpoint, same layout as paper_2603_27156_b200/model.py:
+// "GSRP", u32 version 1, u64 mode, L, D, C, d_in, block count; per block u64 rows,
+// cols, then w (rows × cols) and b (cols) as f64. Blocks: encoder, layer blocks, head.
+struct BlockSpan { size_t off, rows, cols; };
+std::vector<BlockSpan> gsrp_blocks(const gsr::cuda::NetConfig& c) {
+    const int C = c.mode == gsr::cuda::Mode::Alg12 ? 2 : c.groups;
+    const size_t D = static_cast<size_t>(c.hidden), w = D / static_cast<size_t>(C), din = static_cast<size_t>(c.d_in);
+    std::vector<BlockSpan> b;
+    size_t o = 0;
+    b.push_back({o, din, D});
+    o += din * D + D;
+    for (int l = 0; l < c.layers; ++l)
+        for (int i = 0; i < C; ++i) { b.push_back({o, w, w}); o += w * w + w; }
+    b.push_back({o, D, 1});
+    return b;
+}
+
+void write_gsrp(const std::string& path, const std::vector<float>& p, const gsr::cuda::NetConfig& c) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw gsr::ResourceError("cannot write " + path);
+    const auto blocks = gsrp_blocks(c);
+    auto u64 = [&](std::uint64_t v) { f.write(reinterpret_cast<const char*>(&v), 8); };
+    f.write("GSRP", 4);
+    const std::uint32_t ver = 1;
+    f.write(reinterpret_cast<const char*>(&ver), 4);
+    u64(static_cast<std::uint64_t>(c.mode)); u64(static_cast<std::uint64_t>(c.layers)); u64(static_cast<std::uint64_t>(c.hidden));
+    u64(static_cast<std::uint64_t>(c.mode == gsr::cuda::Mode::Alg12 ? 2 : c.groups)); u64(static_cast<std::uint64_t>(c.d_in)); u64(blocks.size());
+    for (const auto& b : blocks) {
+        u64(b.rows); u64(b.cols);
+        for (size_t i = 0; i < b.rows * b.cols + b.cols; ++i) {
+            const double v = p[b.off + i];
+            f.write(reinterpret_cast<const char*>(&v), 8);
+        }
+    }
+}
+
+std::vector<float> read_gsrp(const std::string& path, const gsr::cuda::NetConfig& c, index_t P) {
+    const auto buf = slurp(path);
+    if (buf.size() < 56 || std::memcmp(buf.data(), "GSRP", 4) != 0) throw gsr::FormatError(path + ": bad GSRP magic");
+    if (get_le<std::uint32_t>(buf, 4) != 1) throw gsr::FormatError(path + ": unsupported GSRP version");
+    const std::uint64_t want[5] = {static_cast<std::uint64_t>(c.mode), static_cast<std::uint64_t>(c.layers), static_cast<std::uint64_t>(c.hidden),
+                                   static_cast<std::uint64_t>(c.mode == gsr::cuda::Mode::Alg12 ? 2 : c.groups), static_cast<std::uint64_t>(c.d_in)};
+    for (int i = 0; i < 5; ++i)
+        if (get_le<std::uint64_t>(buf, 8 + 8 * i) != want[i]) throw gsr::ShapeError(path + ": checkpoint config differs from the run config");
+    const auto blocks = gsrp_blocks(c);
+    if (get_le<std::uint64_t>(buf, 48) != blocks.size()) throw gsr::FormatError(path + ": block count mismatch");
+    std::vector<float> p(static_cast<size_t>(P), 0.f);
+    size_t off = 56;
+    for (const auto& b : blocks) {
+        if (off + 16 > buf.size() || get_le<std::uint64_t>(buf, off) != b.rows || get_le<std::uint64_t>(buf, off + 8) != b.cols)
+            throw gsr::FormatError(path + ": block shape mismatch or truncation");
+        off += 16;
+        const size_t cnt = b.rows * b.cols + b.cols;
+        if (off + 8 * cnt > buf.size()) throw gsr::FormatError(path + ": truncated GSRP");
+        for (size_t i = 0; i < cnt; ++i) p[b.off + i] = static_cast<float>(get_le<double>(buf, off + 8 * i));
+        off += 8 * cnt;
+    }
+    if (off != buf.size()) throw gsr::FormatError(path + ": trailing bytes in GSRP");
+    return p;
+}
+
 int usage() {
     std::cerr << "usage: gsrnet-cuda train --graph G.gsrg --nodes N.gsrn [--model gsrc|gsr|baseline] [--layers L] [--hidden D]\n"
                  "                        [--groups C] [--k K] [--epochs E] [--lr LR] [--norm none|row_mean|sym]\n"
-                 "                        [--precision fp32|tf32] [--seed S] [--params init.f32] [--report out.jsonl] [--device I]\n";
+                 "                        [--precision fp32|tf32] [--seed S] [--params init.f32] [--resume in.gsrp]\n"
+                 "                        [--checkpoint out.gsrp] [--report out.jsonl] [--device I]\n";
     return 1;
 }
 
@@ -183,7 +246,9 @@ int run(int argc, char** argv) {
     ctx.init_model(c);
     const index_t P = ctx.num_params();
     std::vector<float> p;
-    if (a.count("params")) {
+    if (a.count("resume")) {
+        p = read_gsrp(a["resume"], c, P);
+    } else if (a.count("params")) {
         const auto b = slurp(a["params"]);
         if (b.size() != 4 * static_cast<size_t>(P)) throw gsr::ShapeError("--params: expected " + std::to_string(P) + " f32 values");
         p.resize(static_cast<size_t>(P));
@@ -213,11 +278,13 @@ int run(int argc, char** argv) {
         if (ep > 0) total += t.t_total;
         std::ostringstream s;
         s.precision(9);
-        s << "{\"record\":\"epoch\",\"epoch\":" << ep << ",\"train_loss\":" << last << ",\"t_total\":" << t.t_total
+        s << "{\"record\":\"epoch\",\"epoch\":" << ep << ",\"train_loss\":" << last << ",\"t_forward\":" << t.t_forward
+          << ",\"t_backward\":" << t.t_backward << ",\"t_optimizer\":" << t.t_optimizer << ",\"t_copy\":" << t.t_copy << ",\"t_total\":" << t.t_total
           << ",\"peak_active_bytes\":" << m.peak_active_bytes << ",\"reserved_bytes\":" << m.reserved_bytes
           << ",\"utilization\":" << m.utilization << "}\n";
         *out << s.str();
     }
+    if (a.count("checkpoint")) write_gsrp(a["checkpoint"], ctx.params(), c);
     const gsrc_mem_report m = ctx.memory();
     std::ostringstream s;
     s.precision(9);
