@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
 // Work is spread over all SMs regardless of how skewed the hub degrees are.
 constexpr int kHubSegThreads = 64;
 template <int W>
-__global__ void __launch_bounds__(kHubSegThreads) k_hub_seg_sparse(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
+__global__ void __launch_bounds__(kHubSegThreads, 10) k_hub_seg_sparse(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
     // one thread per segment: ≤ 8 records, 128-bit loads one record ahead, scattered
     // into a private shared row; the block's rows then leave as coalesced warp stores
     constexpr int PL = W + 4;
@@ -942,25 +942,31 @@ __global__ void __launch_bounds__(kHubSegThreads) k_hub_seg_sparse(FastArgs a, c
                 const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
                 const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
                                       rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
-                int mm[16];
-                float old[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    mm[j] = static_cast<int>(__byte_perm(iw[j >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
-                    if (j < k) old[j] = pr[mm[j]];
+                for (int h = 0; h < 16; h += 8) {  // two halves of 8 distinct slots: fewer live registers
+                    int mm[8];
+                    float old[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        mm[j] = static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
+                        if (h + j < k) old[j] = pr[mm[j]];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (h + j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[h + j]));
                 }
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
             }
         }
     }
     __syncwarp();
-    for (int i = 0; i < 32; ++i) {  // warp copies its 32 partial rows out, lanes over columns
-        const int sg = blockIdx.x * kHubSegThreads + wid * 32 + i;
-        if (sg >= nseg) break;
-        const float* src = slot + (wid * 32 + i) * PL;
-        for (int c = lane; c < a.ld; c += 32) Pseg[static_cast<size_t>(sg) * a.ld + c] = src[c];
+    // the warp copies its 32 partial rows out as float4 chunks, lanes over chunks
+    constexpr int CPR = W / 4;  // chunks per row
+    const int sg0 = blockIdx.x * kHubSegThreads + wid * 32;
+    const int nrow = min(32, nseg - sg0), cpr = a.ld >> 2;
+    float* dst = Pseg + static_cast<size_t>(sg0) * a.ld;
+    for (int i = lane; i < nrow * CPR; i += 32) {
+        const int rr = i / CPR, c4 = i % CPR;
+        if (c4 < cpr) *reinterpret_cast<float4*>(dst + rr * a.ld + 4 * c4) = *reinterpret_cast<const float4*>(slot + (wid * 32 + rr) * PL + 4 * c4);
     }
 }
 
@@ -1014,15 +1020,15 @@ __global__ void __launch_bounds__(256) k_hub_fold(FastArgs a, const int* __restr
 #pragma unroll
     for (int q = 0; q < CPL; ++q) z[q] = (lane + 32 * q < a.ld) ? __ldg(Pseg + static_cast<size_t>(s0) * a.ld + lane + 32 * q) : 0.f;
     int s = s0 + 1;
-    for (; s + 8 <= s1; s += 8) {  // eight partial rows in flight, folded in order
-        float p[8][CPL];
+    for (; s + 16 <= s1; s += 16) {  // sixteen partial rows in flight, folded in order
+        float p[16][CPL];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 16; ++i)
 #pragma unroll
             for (int q = 0; q < CPL; ++q)
                 p[i][q] = (lane + 32 * q < a.ld) ? __ldg(Pseg + static_cast<size_t>(s + i) * a.ld + lane + 32 * q) : 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 16; ++i)
 #pragma unroll
             for (int q = 0; q < CPL; ++q) z[q] = __fadd_rn(z[q], p[i][q]);
     }
