@@ -120,6 +120,7 @@ struct gsrc_ctx {
     int norm = 0;
     int *rp = nullptr, *ci = nullptr, *trp = nullptr, *tci = nullptr;
     float *row_f = nullptr, *col_f = nullptr;
+    int2 *ell_f = nullptr, *ell_b = nullptr;  // Dir::ell per direction
     int *hub_f = nullptr, *hub_b = nullptr;   // rows with > kSeg edges (fwd CSR / transpose), fast path
     int nhub_f = 0, nhub_b = 0;
     // their kSeg-edge segments (edge ranges) and each hub row's segment range
@@ -173,7 +174,7 @@ struct gsrc_ctx {
 
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
-        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)seg_f, (void*)seg_b,
+        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)ell_f, (void*)ell_b, (void*)seg_f, (void*)seg_b,
                         (void*)segoff_f, (void*)segoff_b, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
@@ -191,8 +192,8 @@ struct gsrc_ctx {
     const float* Wb(int l, int i) const { return params + off_block(l, i); }
     const float* Bb(int l, int i) const { return cfg.use_bias ? params + off_block(l, i) + static_cast<int64_t>(w) * w : nullptr; }
     // col_f ≡ 1 unless sym_degree; row_f ≡ 1 only for norm none
-    Dir fwd() const { return Dir{rp, ci, row_f, col_f, norm != GSRC_NORM_SYM_DEGREE}; }
-    Dir bwd() const { return Dir{trp, tci, col_f, row_f, norm == GSRC_NORM_NONE}; }
+    Dir fwd() const { return Dir{rp, ci, row_f, col_f, norm != GSRC_NORM_SYM_DEGREE, ell_f}; }
+    Dir bwd() const { return Dir{trp, tci, col_f, row_f, norm == GSRC_NORM_NONE, ell_b}; }
 
     TileArgs tile_base() const {
         TileArgs a;
@@ -773,8 +774,29 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
-        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b, (void*)ctx->seg_f, (void*)ctx->seg_b, (void*)ctx->segoff_f, (void*)ctx->segoff_b})
+        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b, (void*)ctx->seg_f, (void*)ctx->seg_b, (void*)ctx->segoff_f, (void*)ctx->segoff_b,
+                        (void*)ctx->ell_f, (void*)ctx->ell_b})
             if (p) cudaFree(p);
+        // per-row neighbour slots (Dir::ell): edge scale = the direction's edge_f of the neighbour
+        auto ell_table = [&](const std::vector<int>& ptr, const int* idx, const std::vector<float>& ef) {
+            std::vector<int2> t(static_cast<size_t>(n) * kAggSeg, make_int2(-1, 0));
+            for (int64_t r = 0; r < n; ++r) {
+                int2* s = t.data() + static_cast<size_t>(r) * kAggSeg;
+                const int e0 = ptr[static_cast<size_t>(r)], e1 = ptr[static_cast<size_t>(r) + 1];
+                if (e1 - e0 > kAggSeg) { s[0].x = -2; continue; }
+                for (int q = e0; q < e1; ++q) {
+                    float f = ef[static_cast<size_t>(idx[q])];
+                    int bits;
+                    std::memcpy(&bits, &f, sizeof bits);
+                    s[q - e0] = make_int2(idx[q], bits);
+                }
+            }
+            int2* d = dmalloc<int2>(t.size(), &ctx->graph_bytes);
+            CK(cudaMemcpy(d, t.data(), sizeof(int2) * t.size(), cudaMemcpyHostToDevice));
+            return d;
+        };
+        ctx->ell_f = ell_table(rp, col_idx, cf);
+        ctx->ell_b = ell_table(trp, tci.data(), rf);
         ctx->nhub_f = static_cast<int>(hf.size());
         ctx->nhub_b = static_cast<int>(hb.size());
         ctx->hub_f = dmalloc<int>(hf.size(), &ctx->graph_bytes);

@@ -82,6 +82,13 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// next tile's neighbour slots and row scales toward L2 (one bulk request each)
+__device__ __forceinline__ void prefetch_tile_meta(const Dir& d, int tile_next, int n_tiles, int n) {
+    if (tile_next >= n_tiles) return;
+    const int r0 = tile_next * TR, nr = n - r0 < TR ? n - r0 : TR;
+    prefetch_l2_bulk(d.ell + static_cast<size_t>(r0) * kSegF, static_cast<uint32_t>(nr) * kSegF * 8u);
+    if ((nr & 3) == 0) prefetch_l2_bulk(d.out_f + r0, static_cast<uint32_t>(nr) * 4u);
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // ---- TMA (cp.async.bulk.tensor) for the residual / output row tiles ----------
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int r0) {
@@ -151,34 +158,29 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
 // unrolled (one record in flight ahead): the kernel's code must stay small
 // enough for the instruction cache.
 template <int W, int KS>
-__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
+__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv)[kSegF], const float (&sv)[kSegF], int ne, float* Zs, int r) {
     const int k = KS ? KS : a.k;
     const int RB = rec_bytes(k), nv4 = (k + 3) >> 2;
     const bool unit = a.dir.unit_edge != 0;
-    int c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0;
-    const int c0 = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
-    if (ne > 1) c1 = __ldg(a.dir.idx + e0 + 1);
-    if (ne > 2) c2 = __ldg(a.dir.idx + e0 + 2);
-    if (ne > 3) c3 = __ldg(a.dir.idx + e0 + 3);
-    if (ne > 4) c4 = __ldg(a.dir.idx + e0 + 4);
-    if (ne > 5) c5 = __ldg(a.dir.idx + e0 + 5);
-    if (ne > 6) c6 = __ldg(a.dir.idx + e0 + 6);
-    if (ne > 7) c7 = __ldg(a.dir.idx + e0 + 7);
+    int c1 = cv[1], c2 = cv[2], c3 = cv[3], c4 = cv[4], c5 = cv[5], c6 = cv[6], c7 = cv[7];
+    float s1 = sv[1], s2 = sv[2], s3 = sv[3], s4 = sv[4], s5 = sv[5], s6 = sv[6], s7 = sv[7];
     if (ne > 2) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
     if (ne > 3) prefetch_l2(a.rec_in + static_cast<size_t>(c3) * RB);
     const int rbase = r * 32;
     const uint32_t rxx = static_cast<uint32_t>((r & 7) << 2) * 0x01010101u;
-    int cur_c = c0;
+    float cur_s = sv[0];
     tile::SparseRec cur;
-    if (ne > 0) tile::load_rec16(cur, a.rec_in + static_cast<size_t>(c0) * RB, nv4);
+    if (ne > 0) tile::load_rec16(cur, a.rec_in + static_cast<size_t>(cv[0]) * RB, nv4);
 #pragma unroll 1
     for (int u = 0; u < ne; ++u) {
-        const int nc = c1;  // shift register of the remaining neighbour ids
+        const int nc = c1;  // shift registers of the remaining neighbour ids / scales
+        const float ns = s1;
         c1 = c2; c2 = c3; c3 = c4; c4 = c5; c5 = c6; c6 = c7;
+        s1 = s2; s2 = s3; s3 = s4; s4 = s5; s5 = s6; s6 = s7;
         tile::SparseRec nxt = cur;
         if (u + 1 < ne) tile::load_rec16(nxt, a.rec_in + static_cast<size_t>(nc) * RB, nv4);
         if (u + 3 < ne) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
-        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cur_c);
+        const float sc = unit ? 1.f : cur_s;
         const uint32_t iw[4] = {cur.idx.x, cur.idx.y, cur.idx.z, cur.idx.w};
         const float vv[16] = {cur.v[0].x, cur.v[0].y, cur.v[0].z, cur.v[0].w, cur.v[1].x, cur.v[1].y, cur.v[1].z, cur.v[1].w,
                               cur.v[2].x, cur.v[2].y, cur.v[2].z, cur.v[2].w, cur.v[3].x, cur.v[3].y, cur.v[3].z, cur.v[3].w};
@@ -199,54 +201,24 @@ __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, int e0, int ne
         for (int j = 0; j < NJ; ++j)
             if (KS || j < k) Zs[off[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
         cur = nxt;
-        cur_c = nc;
+        cur_s = ns;
     }
 }
 
-// ---- dense row aggregation (regular rows): z = Σ_e sc_e · x[c_e], in CSR order
-template <int W>
-__device__ __forceinline__ void agg_dense_row(const FastArgs& a, int e0, int ne, float* Zs, int r) {
-    const bool unit = a.dir.unit_edge != 0;
-    int c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0;
-    int c0 = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
-    if (ne > 1) c1 = __ldg(a.dir.idx + e0 + 1);
-    if (ne > 2) c2 = __ldg(a.dir.idx + e0 + 2);
-    if (ne > 3) c3 = __ldg(a.dir.idx + e0 + 3);
-    if (ne > 4) c4 = __ldg(a.dir.idx + e0 + 4);
-    if (ne > 5) c5 = __ldg(a.dir.idx + e0 + 5);
-    if (ne > 6) c6 = __ldg(a.dir.idx + e0 + 6);
-    if (ne > 7) c7 = __ldg(a.dir.idx + e0 + 7);
-    // every neighbour row toward L2 first: the per-edge row loads below then
-    // pay L2 latency, not DRAM latency
-    {
-        const int cc[kSegF] = {c0, c1, c2, c3, c4, c5, c6, c7};
+// a row's neighbour slots (Dir::ell): ids (−1 padding, −2 in slot 0 for a hub
+// row) and edge scales, four independent 16 B loads
+__device__ __forceinline__ int load_ell_row(const int2* ell, int row, int (&cv)[kSegF], float (&sv)[kSegF]) {
+    const int4* ep = reinterpret_cast<const int4*>(ell + static_cast<size_t>(row) * kSegF);
+    int ne = 0;
 #pragma unroll
-        for (int u = 1; u < kSegF; ++u)
-            if (u < ne) prefetch_l2_bulk(a.x_in + static_cast<size_t>(cc[u]) * a.ld, a.ld * 4);
-    }
-    float acc[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) acc[q] = 0.f;
-#pragma unroll 1
-    for (int u = 0; u < ne; ++u) {
-        const int c = c0;
-        c0 = c1; c1 = c2; c2 = c3; c3 = c4; c4 = c5; c5 = c6; c6 = c7;
-        const float sc = unit ? 1.f : __ldg(a.dir.edge_f + c);
-        const float* src = a.x_in + static_cast<size_t>(c) * a.ld;
-        float4 x[W / 4];
-#pragma unroll
-        for (int q = 0; q < W / 4; ++q) x[q] = 4 * q < a.ld ? dev::ld4(src + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < W / 4; ++q) {
-            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sc, x[q].x));
-            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sc, x[q].y));
-            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sc, x[q].z));
-            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sc, x[q].w));
-        }
+    for (int q = 0; q < kSegF / 2; ++q) {
+        const int4 v = __ldg(ep + q);
+        cv[2 * q] = v.x; sv[2 * q] = __int_as_float(v.y);
+        cv[2 * q + 1] = v.z; sv[2 * q + 1] = __int_as_float(v.w);
     }
 #pragma unroll
-    for (int q = 0; q < W / 4; ++q)
-        *reinterpret_cast<float4*>(Zs + zo(r, 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    for (int q = 0; q < kSegF; ++q) ne += cv[q] >= 0 ? 1 : 0;
+    return cv[0] == -2 ? -1 : ne;  // −1: hub row
 }
 
 // GS top-k of a row held in a swizzled smem tile → CBSR record.
@@ -402,20 +374,20 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
 }
 
 template <int W, int KIND, int KS>
-__global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_constant__ FastArgs a) {
+__global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* base = reinterpret_cast<float*>(smem_raw);
     if ((smem_u32(base) & 1023u) != 0) __trap();  // UMMA SW128 atoms need 1 KB alignment
     float* Ws = base;
     float* Zs = Ws + Pl::ws;
-    float* Y2 = Zs + Pl::tile;   // BIN
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(KIND));
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int t = threadIdx.x, wid = t >> 5;
     const int n_tiles = (a.n + TR - 1) / TR;
-    constexpr uint32_t TCOLS = KIND == BIN ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+    static_assert(KIND == FWD || KIND == INV, "BIN is k_bin2");
+    constexpr uint32_t TCOLS = W < 32 ? 32 : W;
 
     // transform operand Bᵀ[n][m] (K-major SW128, region stride W·32)
     for (int i = t; i < W * W; i += TR) {
@@ -432,26 +404,21 @@ __global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_c
     tile::tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t tlane = static_cast<uint32_t>(32 * wid) << 16;
-    uint32_t ph0 = 0, ph1 = 0, ph2 = 0;
-    bool dw_pending = false;
+    uint32_t ph0 = 0, ph2 = 0;
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR;
         const int row = row0 + t;
         const bool valid = row < a.n;
-        if (KIND == BIN && dw_pending) {  // previous dW MMA still reads Zs / Y2
-            mbar_wait(&bar[1], ph1);
-            ph1 ^= 1u;
-            tile::tc_fence_after();
-            dw_pending = false;
-        }
         // stage the residual (FWD / INV) and gradient (INV) rows
 
         // residual tile toward L2 now (TMA prefetch); it is TMA-loaded into Zs
         // once the MMA has consumed the A operand
-        if (KIND != BIN && t == 0)
+        if (t == 0) {
 #pragma unroll
             for (int c = 0; c < W; c += 32) tma_prefetch_2d(&a.tm_x, c, row0);
+            prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
+        }
         // ---- aggregation into this thread's row of the A operand
         {
             const int rbase = t * 32, rx = (t & 7) << 2;
@@ -459,28 +426,26 @@ __global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_c
             for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Zs + rbase + ((c ^ rx) & 31) + (c >> 5) * (TR * 32)) = make_float4(0.f, 0.f, 0.f, 0.f);
             float rf = 0.f;
             if (valid) {
-                const int e0 = __ldg(a.dir.ptr + row), e1 = __ldg(a.dir.ptr + row + 1);
+                int cv[kSegF];
+                float sv[kSegF];
+                const int ne = load_ell_row(a.dir.ell, row, cv, sv);
                 rf = __ldg(a.dir.out_f + row);
-                const int ne = e1 - e0;
-                if (ne > kSegF) {  // hub row: canonical segmented sum precomputed by k_hub_*
+                if (ne < 0) {  // hub row: canonical segmented sum precomputed by k_hub_*
                     const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
 #pragma unroll
                     for (int c = 0; c < W; c += 4)
                         if (c < a.ld) *reinterpret_cast<float4*>(Zs + zo(t, c)) = dev::ld4(zh + c);
-                } else if (KIND == BIN) {
-                    agg_dense_row<W>(a, e0, ne, Zs, t);
                 } else {
-                    agg_sparse_row<W, KS>(a, e0, ne, Zs, t);
+                    agg_sparse_row<W, KS>(a, cv, sv, ne, Zs, t);
                 }
             }
-            // Â row scale (BIN also keeps Y in the MN-major layout for dW)
+            // Â row scale
 #pragma unroll
             for (int c = 0; c < W; c += 4) {
                 float4* p = reinterpret_cast<float4*>(Zs + zo(t, c));
                 float4 v = *p;
                 v.x = __fmul_rn(rf, v.x); v.y = __fmul_rn(rf, v.y); v.z = __fmul_rn(rf, v.z); v.w = __fmul_rn(rf, v.w);
                 *p = v;
-                if (KIND == BIN) *reinterpret_cast<float4*>(Y2 + zb(t, c)) = v;
             }
         }
         tile::fence_proxy_async();
@@ -497,15 +462,14 @@ __global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_c
         mbar_wait(&bar[0], ph0);
         ph0 ^= 1u;
         tile::tc_fence_after();
-        if (KIND != BIN) {  // the MMA has read Zs: bring the residual tile in (rows ≥ n read as 0)
-            if (t == 0) {
-                mbar_expect_tx(&bar[2], static_cast<uint32_t>(TR * W * 4));
+        // the MMA has read Zs: bring the residual tile in (rows ≥ n read as 0)
+        if (t == 0) {
+            mbar_expect_tx(&bar[2], static_cast<uint32_t>(TR * W * 4));
 #pragma unroll
-                for (int c = 0; c < W; c += 32) tma_load_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), &bar[2], c, row0);
-            }
-            mbar_wait(&bar[2], ph2);
-            ph2 ^= 1u;
+            for (int c = 0; c < W; c += 32) tma_load_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), &bar[2], c, row0);
         }
+        mbar_wait(&bar[2], ph2);
+        ph2 ^= 1u;
 
         // ---- epilogue: this thread's accumulator row (TMEM lane = tile row)
 #pragma unroll
@@ -523,159 +487,37 @@ __global__ void __launch_bounds__(TR, KIND == BIN ? 2 : 4) k_fast(const __grid_c
                     o[j] = hv;
                 }
                 float4* rp = reinterpret_cast<float4*>(Zs + zo(t, c));
-                if (KIND != BIN) {
-                    const float4 R = *rp;
-                    if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
-                    else { o[0] = __fsub_rn(R.x, o[0]); o[1] = __fsub_rn(R.y, o[1]); o[2] = __fsub_rn(R.z, o[2]); o[3] = __fsub_rn(R.w, o[3]); }
-                }
-                *rp = make_float4(o[0], o[1], o[2], o[3]);  // output row: TMA store source, GS input / masked-scatter h
+                const float4 R = *rp;
+                if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
+                else { o[0] = __fsub_rn(R.x, o[0]); o[1] = __fsub_rn(R.y, o[1]); o[2] = __fsub_rn(R.z, o[2]); o[3] = __fsub_rn(R.w, o[3]); }
+                *rp = make_float4(o[0], o[1], o[2], o[3]);  // output row: TMA store source and GS input
             }
         }
-        if (KIND != BIN) {  // output tile back in place by TMA (rows ≥ n clipped)
-            tile::fence_proxy_async();
-            __syncthreads();
-            if (t == 0) {
+        // output tile back in place by TMA (rows ≥ n clipped)
+        tile::fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
 #pragma unroll
-                for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), c, row0);
-                tma_store_commit();
-            }
+            for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), c, row0);
+            tma_store_commit();
         }
         if (KIND == FWD && a.gs_out && valid) {
             gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
         }
-        if (KIND != BIN && t == 0) tma_store_wait_read();  // Zs is rewritten by the next tile
-        if (KIND == BIN && valid) {
-            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
-            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
-            const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
-            // the mask columns of a row are distinct: all loads first, then the stores
-            int col[16];
-            float v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                col[j] = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                if (j < a.k_m) v[j] = Zs[zo(t, col[j])];
-            }
-            for (int p = 0; p < a.ndst; ++p) {
-                float* d = a.dst[p] + static_cast<size_t>(row) * a.ld;
-                float o[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) if (j < a.k_m) o[j] = d[col[j]];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) if (j < a.k_m) d[col[j]] = __fadd_rn(o[j], v[j]);
-            }
-        }
-        if (KIND == BIN) {
-            // S = scatter(V, I) of this row (the block's sparse input) over its own
-            // h row, in the MN-major layout: dW += Sᵀ·Y (A = Sᵀ, B = Y2)
-#pragma unroll
-            for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Zs + zb(t, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) {
-                const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
-                const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
-                const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
-                const float* rv = reinterpret_cast<const float*>(rc + rec_kh(a.k_m));
-                for (int j = 0; j < a.k_m; ++j) Zs[zb(t, static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu))] = rv[j];
-            }
-            tile::fence_proxy_async();
-            __syncthreads();
-            if (t == 0) {
-                tile::tc_fence_after();
-                const uint32_t sa = smem_u32(Zs), ya = smem_u32(Y2);
-                const bool first = tile_i == static_cast<int>(blockIdx.x);
-#pragma unroll
-                for (int kk = 0; kk < TR / 8; ++kk)
-                    umma(tmem + W, desc_mn32(sa + kk * 1024), desc_mn32(ya + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
-                tile::umma_commit(&bar[1]);
-            }
-            dw_pending = true;
-        }
+        if (t == 0) tma_store_wait_read();  // Zs is rewritten by the next tile
         tile::tc_fence_before();
         __syncthreads();
-    }
-    if (KIND == BIN) {
-        if (dw_pending) {
-            mbar_wait(&bar[1], ph1);
-            tile::tc_fence_after();
-        }
-        // per-CTA dW partial: TMEM lane m, columns W + n (every CTA writes its slot)
-        const int plen = a.w * a.w + a.w;
-        double* pp = a.part + static_cast<size_t>(blockIdx.x) * plen;
-        const bool any = static_cast<int>(blockIdx.x) < n_tiles;
-#pragma unroll
-        for (int c0 = 0; c0 < W; c0 += 16) {
-            float v[16];
-            tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(W + c0), v);
-            const int m = t;
-            if (m < a.w) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < a.w) pp[m * a.w + c0 + j] = any ? static_cast<double>(v[j]) : 0.0;
-            }
-        }
-        if (t < a.w) pp[a.w * a.w + t] = 0.0;  // db: k_colsum (bias only)
     }
     tile::tc_fence_before();
     __syncthreads();
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
 }
 
-// ---- BIN with two threads per row --------------------------------------------
+// ---- BIN: input gradient and dW, two threads per row ------------------------
 // The dense transposed aggregation gathers a full neighbour row (4w bytes) per
-// edge; with one thread per row only one edge fits in registers at a time.
-// Here threads t and t + 128 share tile row t & 127, each owning one column
-// half: per thread an edge is w/8 float4 loads, two edges are in flight, and
-// the CTA has 8 warps. Everything else is the BIN kind of k_fast.
-template <int W>
-__device__ __forceinline__ void agg_dense_half(const FastArgs& a, int e0, int ne, float* Zs, int r, int hf) {
-    constexpr int HW = W / 2, NQ = HW / 4;
-    const bool unit = a.dir.unit_edge != 0;
-    const int cbase = hf * HW;
-    float acc[HW];
-#pragma unroll
-    for (int q = 0; q < HW; ++q) acc[q] = 0.f;
-    int u = 0;
-    int cn = ne > 0 ? __ldg(a.dir.idx + e0) : 0;
-    int cn2 = ne > 1 ? __ldg(a.dir.idx + e0 + 1) : 0;
-#pragma unroll 1
-    for (; u < ne; u += 2) {  // two edges per round, CSR order kept in the adds
-        const int ca = cn, cb = cn2;
-        const bool hb = u + 1 < ne;
-        cn = u + 2 < ne ? __ldg(a.dir.idx + e0 + u + 2) : 0;
-        cn2 = u + 3 < ne ? __ldg(a.dir.idx + e0 + u + 3) : 0;
-        const float sa = unit ? 1.f : __ldg(a.dir.edge_f + ca);
-        const float sb = (unit || !hb) ? 1.f : __ldg(a.dir.edge_f + cb);
-        float4 xa[NQ], xb[NQ];
-        const float* pa = a.x_in + static_cast<size_t>(ca) * a.ld + cbase;
-        const float* pb = a.x_in + static_cast<size_t>(cb) * a.ld + cbase;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const bool ok = cbase + 4 * q < a.ld;
-            xa[q] = ok ? dev::ld4(pa + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            xb[q] = (ok && hb) ? dev::ld4(pb + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sa, xa[q].x));
-            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sa, xa[q].y));
-            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sa, xa[q].z));
-            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sa, xa[q].w));
-        }
-        if (hb) {
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(sb, xb[q].x));
-                acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(sb, xb[q].y));
-                acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(sb, xb[q].z));
-                acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(sb, xb[q].w));
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-        *reinterpret_cast<float4*>(Zs + zo(r, cbase + 4 * q)) = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-}
-
+// edge: an 8-lane group per row makes each neighbour-row load whole 128 B
+// lines; the epilogue gives threads t and t + 128 one column half each of tile
+// row t & 127. The CTA has 8 warps.
 template <int W>
 __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
@@ -718,6 +560,11 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             tile::tc_fence_after();
             dw_pending = false;
         }
+        if (tid == 0) {  // next tile's slots; this tile's mask records (read after the MMA issue)
+            prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
+            const int nr = a.n - row0 < TR ? a.n - row0 : TR;
+            prefetch_l2_bulk(a.mrec + static_cast<size_t>(row0) * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+        }
         // ---- Y = Âᵀ·x_in, gathered cooperatively: an 8-lane group per row, lane
         // q owning the 16 B column chunks q and q + 8 (W = 64), so every
         // neighbour-row load is four whole 128 B lines per warp instruction
@@ -727,38 +574,31 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             constexpr int NP = TR / 32;  // passes of 32 rows
             const int grp = tid >> 3, q = tid & 7;
             const bool unit = a.dir.unit_edge != 0;
-            // the CSR metadata of all passes first (row range → neighbour ids →
-            // edge scales): three dependent latencies per tile, not per pass
-            int e0v[NP], nrv[NP];
-            float rfv[NP];
-            bool hubv[NP];
+            // the neighbour slots of all passes first (Dir::ell: one row-addressed
+            // load per lane, no row_ptr → col_idx → edge_f chain); lane q holds slot q
+            int mycv[NP];
+            float myscv[NP], rfv[NP];
 #pragma unroll
             for (int ps = 0; ps < NP; ++ps) {
                 const int rw = row0 + ps * 32 + grp;
-                e0v[ps] = 0; nrv[ps] = 0; rfv[ps] = 0.f;
+                int2 e = make_int2(-1, 0);
+                rfv[ps] = 0.f;
                 if (rw < a.n) {
-                    e0v[ps] = __ldg(a.dir.ptr + rw);
-                    nrv[ps] = __ldg(a.dir.ptr + rw + 1) - e0v[ps];
+                    e = __ldg(a.dir.ell + static_cast<size_t>(rw) * kSegF + q);
                     rfv[ps] = __ldg(a.dir.out_f + rw);
                 }
-                hubv[ps] = nrv[ps] > kSegF;
-                if (hubv[ps]) nrv[ps] = 0;
+                mycv[ps] = e.x;
+                myscv[ps] = __int_as_float(e.y);
             }
-            int mycv[NP];
-#pragma unroll
-            for (int ps = 0; ps < NP; ++ps) mycv[ps] = q < nrv[ps] ? __ldg(a.dir.idx + e0v[ps] + q) : 0;
-            float myscv[NP];
-#pragma unroll
-            for (int ps = 0; ps < NP; ++ps) myscv[ps] = (!unit && q < nrv[ps]) ? __ldg(a.dir.edge_f + mycv[ps]) : 1.f;
 #pragma unroll 1
             for (int pass = 0; pass < NP; ++pass) {
                 const int r = pass * 32 + grp, rw = row0 + r;
-                int nr = 0, myc = 0;
+                int myc = -1;
                 float mysc = 1.f, rfr = 0.f;
-                bool hub = false;
 #pragma unroll
                 for (int ps = 0; ps < NP; ++ps)
-                    if (ps == pass) { nr = nrv[ps]; myc = mycv[ps]; mysc = myscv[ps]; rfr = rfv[ps]; hub = hubv[ps]; }
+                    if (ps == pass) { myc = mycv[ps]; mysc = myscv[ps]; rfr = rfv[ps]; }
+                const bool hub = __shfl_sync(0xffffffffu, myc, 0, 8) == -2;
                 float4 acc[NCH];
 #pragma unroll
                 for (int h = 0; h < NCH; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -770,18 +610,20 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
                 }
                 // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
                 float4 x[kSegF][NCH];
+                bool ok[kSegF];
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
                     const int c = __shfl_sync(0xffffffffu, myc, u, 8);
+                    ok[u] = c >= 0;  // slots are filled in CSR order, −1 after the last edge
 #pragma unroll
                     for (int h = 0; h < NCH; ++h)
-                        x[u][h] = (u < nr && 32 * h + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 32 * h + 4 * q)
-                                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                        x[u][h] = (ok[u] && 32 * h + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 32 * h + 4 * q)
+                                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
-                    const float sc = __shfl_sync(0xffffffffu, mysc, u, 8);
-                    if (u < nr) {
+                    const float sc = unit ? 1.f : __shfl_sync(0xffffffffu, mysc, u, 8);
+                    if (ok[u]) {
 #pragma unroll
                         for (int h = 0; h < NCH; ++h) {
                             acc[h].x = __fadd_rn(acc[h].x, __fmul_rn(sc, x[u][h].x));
@@ -1123,7 +965,7 @@ int occupancy() {
         const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(KIND) + 1024);  // + per-CTA reserved smem
         const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
         const int by_regs = 65536 / (regs * TR);
-        constexpr int tcols = KIND == BIN ? (2 * W < 64 ? 64 : 2 * W) : (W < 32 ? 32 : W);
+        constexpr int tcols = W < 32 ? 32 : W;
         occ = by_smem < by_regs ? by_smem : by_regs;
         if (occ > 512 / tcols) occ = 512 / tcols;
         if (occ > 8) occ = 8;
@@ -1183,7 +1025,7 @@ template <int W>
 cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {set_attr<W, FWD, 0>(), set_attr<W, FWD, 8>(), set_attr<W, FWD, 16>(), set_attr<W, INV, 0>(), set_attr<W, INV, 8>(),
-                          set_attr<W, INV, 16>(), set_attr<W, BIN, 0>(),
+                          set_attr<W, INV, 16>(),
                           cudaFuncSetAttribute(k_bin2<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
         if (r != cudaSuccess) e = r;
     return e;

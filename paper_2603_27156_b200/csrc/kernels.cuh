@@ -37,6 +37,11 @@ struct Dir {
     const float* out_f = nullptr;
     const float* edge_f = nullptr;
     int unit_edge = 0;   // edge_f ≡ 1 (multiplication by 1 is exact: skipped)
+    // fast path: kAggSeg {neighbour, edge scale bits} slots per row in CSR order,
+    // −1 padding after the last edge; a row with > kAggSeg edges (hub) has −2 in
+    // slot 0. Row-addressed, so a tile's neighbour ids need no row_ptr → col_idx →
+    // edge_f chain of dependent loads.
+    const int2* ell = nullptr;
 };
 
 enum Agg : int { AGG_SPARSE = 0, AGG_DENSE = 1, AGG_DENSE_RELU = 2, AGG_NONE = 3 };
