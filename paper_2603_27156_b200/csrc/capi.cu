@@ -121,12 +121,13 @@ struct gsrc_ctx {
     int *rp = nullptr, *ci = nullptr, *trp = nullptr, *tci = nullptr;
     float *row_f = nullptr, *col_f = nullptr;
     int2 *ell_f = nullptr, *ell_b = nullptr;  // Dir::ell per direction
-    int *hub_f = nullptr, *hub_b = nullptr;   // rows with > kSeg edges (fwd CSR / transpose), fast path
-    int nhub_f = 0, nhub_b = 0;
+    int nhub_f = 0, nhub_b = 0;  // rows with > kSeg edges (fwd CSR / transpose), fast path
     // their kSeg-edge segments (edge ranges) and each hub row's segment range
-    int2 *seg_f = nullptr, *seg_b = nullptr;
-    int *segoff_f = nullptr, *segoff_b = nullptr;
-    int nseg_f = 0, nseg_b = 0;
+    int4* item_f = nullptr;  // sparse hub work items (launch_hub_rows)
+    int* hcnt_f = nullptr;   // per hub: chunks finished (self-resetting)
+    int2* seg_b = nullptr;   // dense hub segments {lo, hi} (launch_hub_dense)
+    int *hub_b = nullptr, *segoff_b = nullptr;
+    int nseg_f = 0, nseg_b = 0, nitem_f = 0;
     size_t graph_bytes = 0;
 
     // persistent: model state
@@ -174,8 +175,8 @@ struct gsrc_ctx {
 
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
-        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)hub_f, (void*)hub_b, (void*)ell_f, (void*)ell_b, (void*)seg_f, (void*)seg_b,
-                        (void*)segoff_f, (void*)segoff_b, (void*)params, (void*)grads,
+        for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)ell_f, (void*)ell_b, (void*)item_f, (void*)seg_b, (void*)hub_b, (void*)segoff_b,
+                        (void*)hcnt_f, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
@@ -284,9 +285,15 @@ struct gsrc_ctx {
     void run_hub(bool sparse, const FastArgs& f, bool transpose) {
         const int nh = transpose ? nhub_b : nhub_f;
         if (!nh) return;
-        CK(launch_hub_segs(sparse, f, transpose ? seg_b : seg_f, transpose ? nseg_b : nseg_f, transpose ? hub_b : hub_f,
-                           transpose ? segoff_b : segoff_f, nh, Pseg, stream));
-        launches += 2;
+        if (sparse && !transpose) {
+            CK(launch_hub_rows(f, item_f, nitem_f, hcnt_f, Pseg, stream));
+            ++launches;
+        } else if (!sparse && transpose) {
+            CK(launch_hub_dense(f, seg_b, nseg_b, hub_b, segoff_b, nhub_b, Pseg, stream));
+            launches += 2;
+        } else {
+            throw Fail(GSRC_ERR_CONFIG, "hub pre-pass: unsupported direction");
+        }
     }
     void run_fast(int kind, const FastArgs& f) {
         CK(launch_fast(kind, f, stream, &last_grid));
@@ -774,7 +781,7 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
-        for (void* p : {(void*)ctx->hub_f, (void*)ctx->hub_b, (void*)ctx->seg_f, (void*)ctx->seg_b, (void*)ctx->segoff_f, (void*)ctx->segoff_b,
+        for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
                         (void*)ctx->ell_f, (void*)ctx->ell_b})
             if (p) cudaFree(p);
         // per-row neighbour slots (Dir::ell): edge scale = the direction's edge_f of the neighbour
@@ -799,27 +806,43 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         ctx->ell_b = ell_table(trp, tci.data(), rf);
         ctx->nhub_f = static_cast<int>(hf.size());
         ctx->nhub_b = static_cast<int>(hb.size());
-        ctx->hub_f = dmalloc<int>(hf.size(), &ctx->graph_bytes);
-        ctx->hub_b = dmalloc<int>(hb.size(), &ctx->graph_bytes);
-        if (!hf.empty()) CK(cudaMemcpy(ctx->hub_f, hf.data(), sizeof(int) * hf.size(), cudaMemcpyHostToDevice));
-        if (!hb.empty()) CK(cudaMemcpy(ctx->hub_b, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
-        auto seg_table = [&](const std::vector<int>& hubs, const std::vector<int>& ptr, int2*& segs, int*& off, int& nseg) {
-            std::vector<int2> sv;
-            std::vector<int> ov(hubs.size() + 1, 0);
+        auto hub_table = [&](const std::vector<int>& hubs, const std::vector<int>& ptr, int chunk, int4*& items, int& nitem, int*& cnt, int& nseg) {
+            std::vector<int4> iv;
+            int total = 0;
             for (size_t h = 0; h < hubs.size(); ++h) {
+                const int r = hubs[h], e0 = ptr[static_cast<size_t>(r)], e1 = ptr[static_cast<size_t>(r) + 1];
+                const int ns = (e1 - e0 + kAggSeg - 1) / kAggSeg;
+                for (int c0 = 0; c0 < ns; c0 += chunk) {
+                    iv.push_back(make_int4(r, e0, e1, c0));
+                    iv.push_back(make_int4(static_cast<int>(h), total, 0, 0));
+                }
+                total += ns;
+            }
+            nseg = total;
+            nitem = static_cast<int>(iv.size() / 2);
+            items = dmalloc<int4>(iv.size(), &ctx->graph_bytes);
+            cnt = dmalloc<int>(hubs.size(), &ctx->graph_bytes);
+            if (!iv.empty()) CK(cudaMemcpy(items, iv.data(), sizeof(int4) * iv.size(), cudaMemcpyHostToDevice));
+            if (!hubs.empty()) CK(cudaMemset(cnt, 0, sizeof(int) * hubs.size()));
+        };
+        hub_table(hf, rp, kHubChunk, ctx->item_f, ctx->nitem_f, ctx->hcnt_f, ctx->nseg_f);
+        {  // dense: flattened segments, per-hub first segment
+            std::vector<int2> sv;
+            std::vector<int> ov(hb.size() + 1, 0);
+            for (size_t h = 0; h < hb.size(); ++h) {
                 ov[h] = static_cast<int>(sv.size());
-                const int e0 = ptr[static_cast<size_t>(hubs[h])], e1 = ptr[static_cast<size_t>(hubs[h]) + 1];
+                const int e0 = trp[static_cast<size_t>(hb[h])], e1 = trp[static_cast<size_t>(hb[h]) + 1];
                 for (int lo = e0; lo < e1; lo += kAggSeg) sv.push_back(make_int2(lo, std::min(e1, lo + kAggSeg)));
             }
-            ov[hubs.size()] = static_cast<int>(sv.size());
-            nseg = static_cast<int>(sv.size());
-            segs = dmalloc<int2>(sv.size(), &ctx->graph_bytes);
-            off = dmalloc<int>(ov.size(), &ctx->graph_bytes);
-            if (!sv.empty()) CK(cudaMemcpy(segs, sv.data(), sizeof(int2) * sv.size(), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(off, ov.data(), sizeof(int) * ov.size(), cudaMemcpyHostToDevice));
-        };
-        seg_table(hf, rp, ctx->seg_f, ctx->segoff_f, ctx->nseg_f);
-        seg_table(hb, trp, ctx->seg_b, ctx->segoff_b, ctx->nseg_b);
+            ov[hb.size()] = static_cast<int>(sv.size());
+            ctx->nseg_b = static_cast<int>(sv.size());
+            ctx->seg_b = dmalloc<int2>(sv.size(), &ctx->graph_bytes);
+            ctx->segoff_b = dmalloc<int>(ov.size(), &ctx->graph_bytes);
+            ctx->hub_b = dmalloc<int>(hb.size(), &ctx->graph_bytes);
+            if (!sv.empty()) CK(cudaMemcpy(ctx->seg_b, sv.data(), sizeof(int2) * sv.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ctx->segoff_b, ov.data(), sizeof(int) * ov.size(), cudaMemcpyHostToDevice));
+            if (!hb.empty()) CK(cudaMemcpy(ctx->hub_b, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
+        }
         CK(cudaDeviceSynchronize());  // pageable copies may still be in flight when cudaMemcpy returns
         const bool resize = ctx->n != n;
         ctx->n = n;

@@ -743,75 +743,120 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
 }
 
-// ---- hub rows (deg > kSeg), flattened over segments ---------------------------
+// ---- hub rows (deg > kSeg) ----------------------------------------------------
 // Canonical order for a long row: kSeg-edge segments, each summed from +0 in
-// CSR order, then folded left to right. Pass 1 computes every hub segment of
-// the graph independently (one warp per segment, lanes over columns — dense —
-// or over record slots — sparse), writing its partial row to Pseg; pass 2
-// folds each hub row's partials in order (one warp per row, coalesced rows).
-// Work is spread over all SMs regardless of how skewed the hub degrees are.
-constexpr int kHubSegThreads = 64;
-template <int W>
-__global__ void __launch_bounds__(kHubSegThreads, 10) k_hub_seg_sparse(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
-    // one thread per segment: ≤ 8 records, 128-bit loads one record ahead, scattered
-    // into a private shared row; the block's rows then leave as coalesced warp stores
-    constexpr int PL = W + 4;
-    __shared__ __align__(16) float slot[kHubSegThreads * PL];
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int sgi = blockIdx.x * kHubSegThreads + t;
-    float* pr = slot + t * PL;
+// CSR order, then folded left to right. Sparse rows (FWD / INV): one CTA per
+// work item = (hub row, chunk of ≤ kHubChunk consecutive segments) computes the
+// chunk's segment partials into shared rows, a thread per segment. A row of one
+// chunk is folded right there; a longer row's
+// chunks write their partials to Pseg and the last chunk to finish (an atomic
+// count per hub row, reset by that CTA) folds the whole row from Pseg. The fold
+// order is the same either way, so the result does not depend on which CTA
+// folds. Work is spread over all SMs regardless of how skewed the hub degrees are.
+// one segment (≤ kSeg records) of a sparse hub row into the private row pr:
+// 128-bit record loads one ahead, two 8-slot halves per record
+__device__ __forceinline__ void hub_seg_sparse(const FastArgs& a, int lo, int ne, float* pr) {
+    const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
+    const bool unit = a.dir.unit_edge != 0;
+    int cs[kSegF];
 #pragma unroll
-    for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (sgi < nseg) {
-        const int2 se = __ldg(segs + sgi);
-        const int lo = se.x, ne = se.y - se.x;
-        const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
-        const bool unit = a.dir.unit_edge != 0;
-        int cs[kSegF];
+    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
 #pragma unroll
-        for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
+    for (int u = 1; u < kSegF; ++u)
+        if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
+    tile::SparseRec buf[2];
+    tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
 #pragma unroll
-        for (int u = 1; u < kSegF; ++u)
-            if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
-        tile::SparseRec buf[2];
-        tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
+    for (int u = 0; u < kSegF; ++u) {
+        if (u < ne) {
+            if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
+            const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
+            const tile::SparseRec& rc = buf[u & 1];
+            const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
+            const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
+                                  rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
 #pragma unroll
-        for (int u = 0; u < kSegF; ++u) {
-            if (u < ne) {
-                if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
-                const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
-                const tile::SparseRec& rc = buf[u & 1];
-                const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
-                const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
-                                      rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
+            for (int h = 0; h < 16; h += 8) {
+                int mm[8];
+                float old[8];
 #pragma unroll
-                for (int h = 0; h < 16; h += 8) {  // two halves of 8 distinct slots: fewer live registers
-                    int mm[8];
-                    float old[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        mm[j] = static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
-                        if (h + j < k) old[j] = pr[mm[j]];
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (h + j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[h + j]));
+                for (int j = 0; j < 8; ++j) {
+                    mm[j] = static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
+                    if (h + j < k) old[j] = pr[mm[j]];
                 }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (h + j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[h + j]));
             }
         }
     }
-    __syncwarp();
-    // the warp copies its 32 partial rows out as float4 chunks, lanes over chunks
-    constexpr int CPR = W / 4;  // chunks per row
-    const int sg0 = blockIdx.x * kHubSegThreads + wid * 32;
-    const int nrow = min(32, nseg - sg0), cpr = a.ld >> 2;
-    float* dst = Pseg + static_cast<size_t>(sg0) * a.ld;
-    for (int i = lane; i < nrow * CPR; i += 32) {
-        const int rr = i / CPR, c4 = i % CPR;
-        if (c4 < cpr) *reinterpret_cast<float4*>(dst + rr * a.ld + 4 * c4) = *reinterpret_cast<const float4*>(slot + (wid * 32 + rr) * PL + 4 * c4);
-    }
 }
 
+template <int W>
+__global__ void __launch_bounds__(kHubChunk) k_hub_rows(FastArgs a, const int4* __restrict__ items, int* __restrict__ cnt,
+                                                                       float* __restrict__ Pseg) {
+    constexpr int PL = W + 4, CH = kHubChunk, NT = CH;
+    __shared__ __align__(16) float slot[CH * PL];
+    __shared__ int last;
+    const int tid = threadIdx.x;
+    // work item: {row, first edge, end edge, first segment of the chunk}, {hub index, row's first partial}
+    const int4 ia = __ldg(items + 2 * blockIdx.x), ib = __ldg(items + 2 * blockIdx.x + 1);
+    const int r = ia.x, e0 = ia.y, e1 = ia.z, c0 = ia.w, h = ib.x;
+    const int nseg = (e1 - e0 + kSegF - 1) / kSegF;
+    const int ns = min(CH, nseg - c0);
+    float* pr = slot + tid * PL;
+#pragma unroll
+    for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < ns) {
+        const int lo = e0 + (c0 + tid) * kSegF;
+        hub_seg_sparse(a, lo, min(kSegF, e1 - lo), pr);
+    }
+    __syncthreads();
+    const int ld = a.ld;
+    if (nseg <= CH) {  // the whole row is here: fold left to right
+        for (int col = tid; col < ld; col += NT) {
+            float z = slot[col];
+            for (int j = 1; j < ns; ++j) z = __fadd_rn(z, slot[j * PL + col]);
+            a.Zh[static_cast<size_t>(r) * ld + col] = z;
+        }
+        return;
+    }
+    // a chunk of a longer row: partials out, then the last chunk folds the row
+    const int s0 = ib.y;
+    float* P = Pseg + static_cast<size_t>(s0 + c0) * ld;
+    for (int i = tid; i < ns * (ld >> 2); i += NT) {
+        const int rr = i / (ld >> 2), c4 = i % (ld >> 2);
+        *reinterpret_cast<float4*>(P + static_cast<size_t>(rr) * ld + 4 * c4) = *reinterpret_cast<const float4*>(slot + rr * PL + 4 * c4);
+    }
+    __syncthreads();
+    if (tid == 0) {  // the barrier orders the CTA's partial stores before this release
+        __threadfence();
+        const int nch = (nseg + CH - 1) / CH;
+        last = atomicAdd(cnt + h, 1) == nch - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const float* Pr = Pseg + static_cast<size_t>(s0) * ld;
+    for (int col = tid; col < ld; col += NT) {
+        float z = __ldcg(Pr + col);
+        int s = 1;
+        for (; s + 16 <= nseg; s += 16) {  // sixteen partials in flight, folded in order
+            float p[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) p[i] = __ldcg(Pr + static_cast<size_t>(s + i) * ld + col);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z = __fadd_rn(z, p[i]);
+        }
+        for (; s < nseg; ++s) z = __fadd_rn(z, __ldcg(Pr + static_cast<size_t>(s) * ld + col));
+        a.Zh[static_cast<size_t>(r) * ld + col] = z;
+    }
+    if (tid == 0) cnt[h] = 0;  // ready for the next launch
+}
+
+// dense hub rows (BIN): flattened, one warp per segment over all hub segments
+// of the graph (every neighbour row one coalesced load; at the gather's
+// roofline), then one warp per hub row folds its partials in order.
 template <int W>
 __global__ void __launch_bounds__(256) k_hub_seg_dense(FastArgs a, const int2* __restrict__ segs, int nseg, float* __restrict__ Pseg) {
     // one warp per segment, lanes over columns: every neighbour row is one coalesced load
@@ -1109,17 +1154,23 @@ cudaError_t launch_gs_tma(const GsArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_hub_segs(bool sparse, const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub,
-                            float* Pseg, cudaStream_t s) {
+cudaError_t launch_hub_rows(const FastArgs& a, const int4* items, int nitem, int* cnt, float* Pseg, cudaStream_t s) {
+    if (nitem == 0) return cudaSuccess;
+    if (a.w <= 32) fast::k_hub_rows<32><<<nitem, kHubChunk, 0, s>>>(a, items, cnt, Pseg);
+    else if (a.w <= 64) fast::k_hub_rows<64><<<nitem, kHubChunk, 0, s>>>(a, items, cnt, Pseg);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hub_dense(const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub, float* Pseg,
+                             cudaStream_t s) {
     if (nhub == 0) return cudaSuccess;
-    const int gsp = (nseg + fast::kHubSegThreads - 1) / fast::kHubSegThreads, gsd = (nseg + 7) / 8, gf = (nhub + 7) / 8;
+    const int gs = (nseg + 7) / 8, gf = (nhub + 7) / 8;
     if (a.w <= 32) {
-        if (sparse) fast::k_hub_seg_sparse<32><<<gsp, fast::kHubSegThreads, 0, s>>>(a, segs, nseg, Pseg);
-        else fast::k_hub_seg_dense<32><<<gsd, 256, 0, s>>>(a, segs, nseg, Pseg);
+        fast::k_hub_seg_dense<32><<<gs, 256, 0, s>>>(a, segs, nseg, Pseg);
         fast::k_hub_fold<32><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
     } else if (a.w <= 64) {
-        if (sparse) fast::k_hub_seg_sparse<64><<<gsp, fast::kHubSegThreads, 0, s>>>(a, segs, nseg, Pseg);
-        else fast::k_hub_seg_dense<64><<<gsd, 256, 0, s>>>(a, segs, nseg, Pseg);
+        fast::k_hub_seg_dense<64><<<gs, 256, 0, s>>>(a, segs, nseg, Pseg);
         fast::k_hub_fold<64><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
     } else {
         return cudaErrorInvalidValue;

@@ -122,8 +122,15 @@ cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld);
 cudaError_t init_fast_attributes();
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out);
 // hub rows flattened over their kSeg-edge segments: partials, then ordered fold
-cudaError_t launch_hub_segs(bool sparse, const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub,
-                            float* Pseg, cudaStream_t s);
+// hub rows of the fast path. Sparse (forward direction): work items of two
+// int4 each, {row, first edge, end edge, first segment of the chunk}, {hub
+// index, the row's first partial in Pseg}; chunks of kHubChunk segments;
+// cnt[nhub] zeroed (left zeroed by every launch). Dense (transpose): the
+// flattened segment list {lo, hi} of all hub rows, then a fold per hub row.
+constexpr int kHubChunk = 64;
+cudaError_t launch_hub_rows(const FastArgs& a, const int4* items, int nitem, int* cnt, float* Pseg, cudaStream_t s);
+cudaError_t launch_hub_dense(const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub, float* Pseg,
+                             cudaStream_t s);
 cudaError_t launch_colsum(const float* G, int n, int w, int ld, double* part, int* grid_out, cudaStream_t s);
 
 // GS top-k of (sum of) planes: u = p0 + p1 + ... (left to right), records out.
