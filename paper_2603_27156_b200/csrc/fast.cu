@@ -72,7 +72,7 @@ struct Plan {
     // stride from Zs); rows m ≥ W read past Zs into Y2 and land in TMEM lanes
     // that are never read, so Zs + 4 atoms must stay inside the allocation.
     static constexpr int bin_tail = 2 * tile > 4 * TR * 32 ? 2 * tile : 4 * TR * 32;
-    static constexpr int floats(int kind) { return kind == BIN ? ws + bin_tail : ws + tile; }
+    static constexpr int floats(int kind) { return kind == BIN ? ws + tile + bin_tail : ws + tile; }
     static constexpr size_t bytes(int kind) { return static_cast<size_t>(floats(kind) + 64) * sizeof(float); }
 };
 
@@ -526,8 +526,9 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     float* base = reinterpret_cast<float*>(smem_raw);
     if ((smem_u32(base) & 1023u) != 0) __trap();
     float* Ws = base;
-    float* Zs = Ws + Pl::ws;
-    float* Y2 = Zs + Pl::tile;
+    float* Zs = Ws + Pl::ws;     // Y (K-major, MMA A), then du for the TMA reduce-add
+    float* S2 = Zs + Pl::tile;   // S (BASE32B): the dW MMA's A = Sᵀ reads four atoms, into Y2
+    float* Y2 = S2 + Pl::tile;   // Y (BASE32B), the dW MMA's B
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(BIN));
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
     const int tid = threadIdx.x, wid = tid >> 5;
@@ -550,6 +551,10 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     const uint32_t tlane = static_cast<uint32_t>(32 * (wid & 3)) << 16;
     uint32_t ph0 = 0, ph1 = 0;
     bool dw_pending = false;
+    if (tid == 0 && static_cast<int>(blockIdx.x) < n_tiles) {  // the first tile's mask records
+        const int nr = a.n - static_cast<int>(blockIdx.x) * TR < TR ? a.n - static_cast<int>(blockIdx.x) * TR : TR;
+        prefetch_l2_bulk(a.mrec + static_cast<size_t>(blockIdx.x) * TR * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+    }
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR, row = row0 + t;
@@ -560,11 +565,42 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             tile::tc_fence_after();
             dw_pending = false;
         }
-        if (tid == 0) {  // next tile's slots; this tile's mask records (read after the MMA issue)
-            prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
-            const int nr = a.n - row0 < TR ? a.n - row0 : TR;
-            prefetch_l2_bulk(a.mrec + static_cast<size_t>(row0) * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+        const int tnext = tile_i + static_cast<int>(gridDim.x);
+        if (tid == 0) {  // the next tile's slots and mask records
+            prefetch_tile_meta(a.dir, tnext, n_tiles, a.n);
+            if (tnext < n_tiles) {
+                const int nr = a.n - tnext * TR < TR ? a.n - tnext * TR : TR;
+                prefetch_l2_bulk(a.mrec + static_cast<size_t>(tnext) * TR * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+            }
         }
+        // mask record of the row (the block's input records: S and the input-gradient mask)
+        uint32_t iw[4] = {0u, 0u, 0u, 0u};
+        float rv[16];
+        if (valid) {
+            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
+            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
+            iw[0] = iw4.x; iw[1] = iw4.y; iw[2] = iw4.z; iw[3] = iw4.w;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v4 = 4 * q < a.k_m ? *reinterpret_cast<const float4*>(rc + 16 + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                rv[4 * q] = v4.x; rv[4 * q + 1] = v4.y; rv[4 * q + 2] = v4.z; rv[4 * q + 3] = v4.w;
+            }
+        }
+        // ---- S = scatter(V, I) of the row, this thread's half (BASE32B): dW += Sᵀ·Y
+        // (the previous tile's dW MMA has released S2 / Y2)
+#pragma unroll
+        for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(S2 + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t hm = 0u;  // this half's mask columns (mask of a padding / invalid row: empty)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+            if (valid && j < a.k_m && c / HW == hf) {
+                S2[zb(t, c)] = rv[j];
+                hm |= 1u << (c - c_lo);
+            }
+        }
+        if (tid == 0) tma_store_wait_read();  // the previous tile's du (Zs) has been read by its reduce-add
+        __syncthreads();
         // ---- Y = Âᵀ·x_in, gathered cooperatively: an 8-lane group per row, lane
         // q owning the 16 B column chunks q and q + 8 (W = 64), so every
         // neighbour-row load is four whole 128 B lines per warp instruction
@@ -642,6 +678,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             }
         }
         tile::fence_proxy_async();
+        tile::tc_fence_before();
         __syncthreads();
         if (tid == 0) {
             tile::tc_fence_after();
@@ -651,27 +688,14 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
                 umma(tmem, desc_sw128(za + (kk >> 2) * (TR * 128) + (kk & 3) * 32, 16), desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16),
                      idesc<W>(0, 0), kk > 0 ? 1u : 0u);
             tile::umma_commit(&bar[0]);
-        }
-        // mask record of the row (the block's input records: S and the input-gradient mask)
-        uint32_t iw[4] = {0u, 0u, 0u, 0u};
-        float rv[16];
-        if (valid) {
-            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
-            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
-            iw[0] = iw4.x; iw[1] = iw4.y; iw[2] = iw4.z; iw[3] = iw4.w;
+            const uint32_t sa = smem_u32(S2), ya = smem_u32(Y2);
+            const bool first = tile_i == static_cast<int>(blockIdx.x);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 v4 = 4 * q < a.k_m ? *reinterpret_cast<const float4*>(rc + 16 + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                rv[4 * q] = v4.x; rv[4 * q + 1] = v4.y; rv[4 * q + 2] = v4.z; rv[4 * q + 3] = v4.w;
-            }
+            for (int kk = 0; kk < TR / 8; ++kk)
+                umma(tmem + W, desc_mn32(sa + kk * 1024), desc_mn32(ya + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
+            tile::umma_commit(&bar[1]);
         }
-        // this half's mask columns as a bitmask (mask of a padding / invalid row: empty)
-        uint32_t hm = 0u;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-            if (valid && j < a.k_m && c / HW == hf) hm |= 1u << (c - c_lo);
-        }
+        dw_pending = true;
         mbar_wait(&bar[0], ph0);
         ph0 ^= 1u;
         tile::tc_fence_after();
@@ -695,30 +719,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
 #pragma unroll
                 for (int c = 0; c < W; c += 32) tma_reduce_add_2d(&a.tm_dst[p], Zs + (c >> 5) * (TR * 32), c, row0);
             tma_store_commit();
-            tma_store_wait_read();  // Zs is rewritten with S below
         }
-        __syncthreads();
-        // ---- S = scatter(V, I) of the row (BASE32B): dW += Sᵀ·Y
-#pragma unroll
-        for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(Zs + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-            if (valid && j < a.k_m && c / HW == hf) Zs[zb(t, c)] = rv[j];
-        }
-        tile::fence_proxy_async();
-        tile::tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tile::tc_fence_after();
-            const uint32_t sa = smem_u32(Zs), ya = smem_u32(Y2);
-            const bool first = tile_i == static_cast<int>(blockIdx.x);
-#pragma unroll
-            for (int kk = 0; kk < TR / 8; ++kk)
-                umma(tmem + W, desc_mn32(sa + kk * 1024), desc_mn32(ya + kk * 1024), idesc<W>(1, 1), (first && kk == 0) ? 0u : 1u);
-            tile::umma_commit(&bar[1]);
-        }
-        dw_pending = true;
     }
     if (dw_pending) {
         mbar_wait(&bar[1], ph1);
@@ -738,6 +739,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
         }
     }
     if (hf == 0 && t < a.w) pp[a.w * a.w + t] = 0.0;  // db: k_colsum (bias only)
+    if (tid == 0) tma_store_wait_read();  // the last du tile leaves shared memory before exit
     tile::tc_fence_before();
     __syncthreads();
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
