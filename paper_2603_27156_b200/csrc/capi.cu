@@ -152,6 +152,7 @@ struct gsrc_ctx {
     float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr, *Zh = nullptr;
     std::vector<CUtensorMap> xmaps, gmaps;  // TMA maps of the X and G planes (fast path)
     uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
+    std::vector<uint8_t*> rblk;  // fast backward sweep: records of block i's input (rblk[0] = recA, rblk[1] = recB)
     std::vector<uint8_t*> c1, c2;
     std::vector<char> filled;
     double* part = nullptr;
@@ -325,7 +326,8 @@ struct gsrc_ctx {
             ++launches;
         }
     }
-    void fast_inverse(int l, int i, const uint8_t* rec) {
+    // gs_out: GS_k of the reconstructed rows (the lower layer's records)
+    void fast_inverse(int l, int i, const uint8_t* rec, uint8_t* gs_out = nullptr) {
         FastArgs f = fast_base(false);
         f.rec_in = rec;
         run_hub(true, f, false);
@@ -334,8 +336,37 @@ struct gsrc_ctx {
         f.R = plane(X, i);
         f.out = plane(X, i);
         f.tm_x = xmaps[static_cast<size_t>(i)];
+        f.gs_out = gs_out;
+        f.k_gs = k;
         run_fast(1, f);
     }
+    // GSR-C backward of layer l on the fast path. Block i ≥ 1 reads rblk[i] =
+    // GS(y_{i-1}); block 0 reads rblk[0] = GS(Σ_{p≥1} x_p), computed by k_gs
+    // once x_1..x_{C-1} are reconstructed. With `produce`, the INV of block
+    // i ≤ C-2 also writes the GS of its reconstructed rows x_i = the lower
+    // layer's y_i, i.e. rblk[i+1] of layer l-1 (free again: block i+1 of this
+    // layer is done), so the sweep needs no per-block GS recompute. Without
+    // `have` (the first layer of the sweep, or a single-layer call) the
+    // records come from the planes.
+    void fast_layer_backward(int l, bool have, bool produce) {
+        if (!have)
+            for (int i = 1; i < C; ++i) run_gs({plane(X, i - 1)}, rblk[static_cast<size_t>(i)]);
+        for (int i = C - 1; i >= 0; --i) {
+            uint8_t* rec = rblk[static_cast<size_t>(i)];
+            uint8_t* own = produce && i <= C - 2 ? rblk[static_cast<size_t>(i) + 1] : nullptr;
+            if (i == 0) run_gs_groupsum(X, rec);
+            fast_inverse(l, i, rec, own);
+            fast_input_grad(l, i, rec);
+            reduce_block_grads(l, i);
+            if (cfg.use_bias) {
+                CK(launch_colsum(plane(G, i), static_cast<int>(n), w, ld, part, &last_grid, stream));
+                ++launches;
+                CK(launch_reduce_parts(part, last_grid, w, w, grads + off_block(l, i) + static_cast<size_t>(w) * w, 1, stream));
+                ++launches;
+            }
+        }
+    }
+    bool fast_sweep() const { return fast() && cfg.use_weight && cfg.mode == GSRC_MODE_GSRC && C >= 2; }
     void fast_input_grad(int l, int i, const uint8_t* rec) {
         FastArgs b = fast_base(true);
         b.x_in = plane(G, i);
@@ -436,7 +467,10 @@ struct gsrc_ctx {
         run_tile(b);
     }
     void rev_layer_inverse(int l) { for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, false); }
-    void rev_layer_backward(int l) { for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, true); }
+    void rev_layer_backward(int l) {
+        if (fast_sweep()) { fast_layer_backward(l, false, false); return; }
+        for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, true);
+    }
 
     // ---- Algorithms 1-2 --------------------------------------------------------
     void alg12_layer_forward(int l) {
@@ -518,7 +552,10 @@ struct gsrc_ctx {
         ++launches;
         CK(launch_reduce_parts(part, nparts_small, cfg.hidden + 1, cfg.hidden + 1, grads + off_block(cfg.layers, 0), 0, stream));
         ++launches;
-        for (int l = cfg.layers - 1; l >= 0; --l) layer_backward(l);
+        for (int l = cfg.layers - 1; l >= 0; --l) {
+            if (fast_sweep()) fast_layer_backward(l, l < cfg.layers - 1, l > 0);
+            else layer_backward(l);
+        }
         const int elen = cfg.d_in * cfg.hidden + cfg.hidden;
         CK(launch_encoder_bwd(X0, G, static_cast<int>(n), cfg.d_in, cfg.hidden, C, w, ld, part, nparts_small, stream));
         ++launches;
@@ -564,6 +601,7 @@ struct gsrc_ctx {
         size_t total = 0;
         total += 2 * bytes_rounded(pl * C * sizeof(float));               // X, G
         total += 2 * bytes_rounded(rb);                                    // recA, recB
+        if (fast() && C > 2) total += static_cast<size_t>(C - 2) * bytes_rounded(rb);  // rblk[2..C-1]
         total += bytes_rounded(part_len * sizeof(double));
         total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
@@ -577,6 +615,9 @@ struct gsrc_ctx {
         G = arena.lease<float>(pl * C);
         recA = arena.lease<uint8_t>(rb);
         recB = arena.lease<uint8_t>(rb);
+        rblk.assign({recA, recB});
+        if (fast())
+            for (int i = 2; i < C; ++i) rblk.push_back(arena.lease<uint8_t>(rb));
         part = arena.lease<double>(part_len);
         yhat = arena.lease<float>(static_cast<size_t>(n));
         gy = arena.lease<float>(static_cast<size_t>(n));

@@ -501,9 +501,7 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
             for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), c, row0);
             tma_store_commit();
         }
-        if (KIND == FWD && a.gs_out && valid) {
-            gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
-        }
+        if (a.gs_out && valid) gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
         if (t == 0) tma_store_wait_read();  // Zs is rewritten by the next tile
         tile::tc_fence_before();
         __syncthreads();
@@ -1134,7 +1132,7 @@ cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_o
     if (grid_out) *grid_out = 0;
     if (a.n == 0) return cudaSuccess;
     if (kind != fast::BIN && (a.k < 1 || a.k > 16)) return cudaErrorInvalidValue;
-    if (kind == fast::FWD && a.gs_out && (a.k_gs < 1 || a.k_gs > 16)) return cudaErrorInvalidValue;
+    if (a.gs_out && (a.k_gs < 1 || a.k_gs > 16)) return cudaErrorInvalidValue;
     if (a.w <= 32) return fast::launch_w<32>(kind, a, s, grid_out);
     if (a.w <= 64) return fast::launch_w<64>(kind, a, s, grid_out);
     return cudaErrorInvalidValue;

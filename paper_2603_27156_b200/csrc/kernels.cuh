@@ -104,7 +104,7 @@ struct FastArgs {
     int gemm_t = 0;                        // 0: h = Z·W, 1: h = Z·Wᵀ
     const float* R = nullptr;
     float* out = nullptr;                  // FWD / INV: out aliases R (in place), moved by TMA through tm_x
-    std::uint8_t* gs_out = nullptr;
+    std::uint8_t* gs_out = nullptr;        // FWD / INV: GS_k of the output rows (the next block's, or the lower layer's, records)
     int k_gs = 0;
     double* part = nullptr;                // BIN: dW partials [grid][w*w + w]
     const std::uint8_t* mrec = nullptr;    // BIN: mask records
@@ -121,7 +121,6 @@ bool fast_supported(int w, int k);
 cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld);
 cudaError_t init_fast_attributes();
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out);
-// hub rows flattened over their kSeg-edge segments: partials, then ordered fold
 // hub rows of the fast path. Sparse (forward direction): work items of two
 // int4 each, {row, first edge, end edge, first segment of the chunk}, {hub
 // index, the row's first partial in Pseg}; chunks of kHubChunk segments;
