@@ -516,10 +516,10 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
 // edge: an 8-lane group per row makes each neighbour-row load whole 128 B
 // lines; the epilogue gives threads t and t + 128 one column half each of tile
 // row t & 127. The CTA has 8 warps.
-template <int W>
-__global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ FastArgs a) {
+template <int W, int TPR>
+__global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
-    constexpr int NT = 2 * TR, HW = W / 2;
+    constexpr int NT = TPR * TR, HW = W / TPR;  // HW: this thread's epilogue columns
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* base = reinterpret_cast<float*>(smem_raw);
     if ((smem_u32(base) & 1023u) != 0) __trap();
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats(BIN));
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
     const int tid = threadIdx.x, wid = tid >> 5;
-    const int t = tid & (TR - 1), hf = tid >> 7;  // tile row, column half
+    const int t = tid & (TR - 1), hf = tid >> 7;  // tile row, column part
     const int c_lo = hf * HW;
     const int n_tiles = (a.n + TR - 1) / TR;
     constexpr uint32_t TCOLS = 2 * W < 64 ? 64 : 2 * W;
@@ -572,28 +572,21 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             }
         }
         // mask record of the row (the block's input records: S and the input-gradient mask)
-        uint32_t iw[4] = {0u, 0u, 0u, 0u};
-        float rv[16];
-        if (valid) {
-            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
-            const uint4 iw4 = *reinterpret_cast<const uint4*>(rc);
-            iw[0] = iw4.x; iw[1] = iw4.y; iw[2] = iw4.z; iw[3] = iw4.w;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 v4 = 4 * q < a.k_m ? *reinterpret_cast<const float4*>(rc + 16 + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                rv[4 * q] = v4.x; rv[4 * q + 1] = v4.y; rv[4 * q + 2] = v4.z; rv[4 * q + 3] = v4.w;
-            }
-        }
-        // ---- S = scatter(V, I) of the row, this thread's half (BASE32B): dW += Sᵀ·Y
-        // (the previous tile's dW MMA has released S2 / Y2)
+        const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
+        uint4 iw4 = make_uint4(0u, 0u, 0u, 0u);
+        if (valid) iw4 = *reinterpret_cast<const uint4*>(rc);
+        const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
+        // ---- S = scatter(V, I) of the row, this thread's columns (BASE32B): dW += Sᵀ·Y
+        // (the previous tile's dW MMA has released S2 / Y2); values loaded only
+        // for this thread's columns (the row's record is in L1 for its threads)
 #pragma unroll
         for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(S2 + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint32_t hm = 0u;  // this half's mask columns (mask of a padding / invalid row: empty)
+        uint32_t hm = 0u;  // this thread's mask columns (mask of a padding / invalid row: empty)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
             if (valid && j < a.k_m && c / HW == hf) {
-                S2[zb(t, c)] = rv[j];
+                S2[zb(t, c)] = *reinterpret_cast<const float*>(rc + 16 + 4 * j);
                 hm |= 1u << (c - c_lo);
             }
         }
@@ -604,9 +597,11 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
         // neighbour-row load is four whole 128 B lines per warp instruction
         // (not 32 scattered sectors); up to 8 edges of loads in flight per lane.
         {
-            constexpr int NCH = W / 32;  // 16 B chunks per lane: columns 4q (+32)
-            constexpr int NP = TR / 32;  // passes of 32 rows
-            const int grp = tid >> 3, q = tid & 7;
+            constexpr int NCH = (TPR == 2 && W == 64) ? 2 : 1;  // 16 B chunks per lane: columns 4q (+4·LPR)
+            constexpr int LPR = W / 4 / NCH;                    // lanes per row
+            constexpr int RPP = NT / LPR;                       // rows per pass
+            constexpr int NP = TR / RPP;                        // passes
+            const int grp = tid / LPR, q = tid % LPR;
             const bool unit = a.dir.unit_edge != 0;
             // the neighbour slots of all passes first (Dir::ell: one row-addressed
             // load per lane, no row_ptr → col_idx → edge_f chain); lane q holds slot q
@@ -614,11 +609,11 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             float myscv[NP], rfv[NP];
 #pragma unroll
             for (int ps = 0; ps < NP; ++ps) {
-                const int rw = row0 + ps * 32 + grp;
+                const int rw = row0 + ps * RPP + grp;
                 int2 e = make_int2(-1, 0);
                 rfv[ps] = 0.f;
                 if (rw < a.n) {
-                    e = __ldg(a.dir.ell + static_cast<size_t>(rw) * kSegF + q);
+                    if (q < kSegF) e = __ldg(a.dir.ell + static_cast<size_t>(rw) * kSegF + q);
                     rfv[ps] = __ldg(a.dir.out_f + rw);
                 }
                 mycv[ps] = e.x;
@@ -626,13 +621,13 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
             }
 #pragma unroll 1
             for (int pass = 0; pass < NP; ++pass) {
-                const int r = pass * 32 + grp, rw = row0 + r;
+                const int r = pass * RPP + grp, rw = row0 + r;
                 int myc = -1;
                 float mysc = 1.f, rfr = 0.f;
 #pragma unroll
                 for (int ps = 0; ps < NP; ++ps)
                     if (ps == pass) { myc = mycv[ps]; mysc = myscv[ps]; rfr = rfv[ps]; }
-                const bool hub = __shfl_sync(0xffffffffu, myc, 0, 8) == -2;
+                const bool hub = __shfl_sync(0xffffffffu, myc, 0, LPR) == -2;
                 float4 acc[NCH];
 #pragma unroll
                 for (int h = 0; h < NCH; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -640,23 +635,23 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
                     const float* zh = a.Zh + static_cast<size_t>(rw) * a.ld;
 #pragma unroll
                     for (int h = 0; h < NCH; ++h)
-                        if (32 * h + 4 * q < a.ld) acc[h] = dev::ld4(zh + 32 * h + 4 * q);
+                        if (4 * (q + LPR * h) < a.ld) acc[h] = dev::ld4(zh + 4 * (q + LPR * h));
                 }
                 // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
                 float4 x[kSegF][NCH];
                 bool ok[kSegF];
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
-                    const int c = __shfl_sync(0xffffffffu, myc, u, 8);
+                    const int c = __shfl_sync(0xffffffffu, myc, u, LPR);
                     ok[u] = c >= 0;  // slots are filled in CSR order, −1 after the last edge
 #pragma unroll
                     for (int h = 0; h < NCH; ++h)
-                        x[u][h] = (ok[u] && 32 * h + 4 * q < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 32 * h + 4 * q)
+                        x[u][h] = (ok[u] && 4 * (q + LPR * h) < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 4 * (q + LPR * h))
                                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
-                    const float sc = unit ? 1.f : __shfl_sync(0xffffffffu, mysc, u, 8);
+                    const float sc = unit ? 1.f : __shfl_sync(0xffffffffu, mysc, u, LPR);
                     if (ok[u]) {
 #pragma unroll
                         for (int h = 0; h < NCH; ++h) {
@@ -670,8 +665,8 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
 #pragma unroll
                 for (int h = 0; h < NCH; ++h) {  // Â scale; Y in K-major (MMA A) and BASE32B (dW B)
                     const float4 v = make_float4(__fmul_rn(rfr, acc[h].x), __fmul_rn(rfr, acc[h].y), __fmul_rn(rfr, acc[h].z), __fmul_rn(rfr, acc[h].w));
-                    *reinterpret_cast<float4*>(Zs + zo(r, 32 * h + 4 * q)) = v;
-                    *reinterpret_cast<float4*>(Y2 + zb(r, 32 * h + 4 * q)) = v;
+                    *reinterpret_cast<float4*>(Zs + zo(r, 4 * (q + LPR * h))) = v;
+                    *reinterpret_cast<float4*>(Y2 + zb(r, 4 * (q + LPR * h))) = v;
                 }
             }
         }
@@ -700,14 +695,15 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
         // ---- du = mask ⊙ (Y·Wᵀ), this thread's half → Zs: the tile TMA
         // reduce-adds into every destination plane (each element receives one
         // add, so the result is deterministic; off-mask entries add +0)
+        constexpr int CW = HW < 16 ? HW : 16;  // TMEM columns per load
 #pragma unroll
-        for (int c0 = 0; c0 < HW; c0 += 16) {
-            float h[16];
-            tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(c_lo + c0), h);
+        for (int c0 = 0; c0 < HW; c0 += CW) {
+            float h[CW];
+            tmem_ld<CW>(tmem + tlane + static_cast<uint32_t>(c_lo + c0), h);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) h[q] = (hm >> (c0 + q)) & 1u ? h[q] : 0.f;
+            for (int q = 0; q < CW; ++q) h[q] = (hm >> (c0 + q)) & 1u ? h[q] : 0.f;
 #pragma unroll
-            for (int q = 0; q < 16; q += 4)
+            for (int q = 0; q < CW; q += 4)
                 *reinterpret_cast<float4*>(Zs + zo(t, c_lo + c0 + q)) = make_float4(h[q], h[q + 1], h[q + 2], h[q + 3]);
         }
         tile::fence_proxy_async();
@@ -726,13 +722,14 @@ __global__ void __launch_bounds__(2 * TR, 2) k_bin2(const __grid_constant__ Fast
     // per-CTA dW partial: TMEM lane m, columns W + n; each half writes its columns
     const int plen = a.w * a.w + a.w;
     double* pp = a.part + static_cast<size_t>(blockIdx.x) * plen;
+    constexpr int CW2 = HW < 16 ? HW : 16;
 #pragma unroll
-    for (int c0 = 0; c0 < HW; c0 += 16) {
-        float v[16];
-        tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(W + c_lo + c0), v);
+    for (int c0 = 0; c0 < HW; c0 += CW2) {
+        float v[CW2];
+        tmem_ld<CW2>(tmem + tlane + static_cast<uint32_t>(W + c_lo + c0), v);
         if (t < a.w) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
+            for (int j = 0; j < CW2; ++j)
                 if (c_lo + c0 + j < a.w) pp[t * a.w + c_lo + c0 + j] = static_cast<double>(v[j]);
         }
     }
@@ -1035,6 +1032,8 @@ cudaError_t set_attr() {
     return cudaFuncSetAttribute(k_fast<W, KIND, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(KIND)));
 }
 
+constexpr int kBinTPR = 2;  // BIN threads per tile row (epilogue columns W / kBinTPR each)
+
 template <int W>
 int occupancy_bin2() {
     static int occ = 0;
@@ -1043,10 +1042,10 @@ int occupancy_bin2() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, k_bin2<W>);
+        cudaFuncGetAttributes(&fa, k_bin2<W, kBinTPR>);
         const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(BIN) + 1024);
         const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
-        const int by_regs = 65536 / (regs * 2 * TR);
+        const int by_regs = 65536 / (regs * kBinTPR * TR);
         occ = by_smem < by_regs ? by_smem : by_regs;
         const int tcols = 2 * W < 64 ? 64 : 2 * W;
         if (occ > 512 / tcols) occ = 512 / tcols;
@@ -1062,7 +1061,7 @@ cudaError_t launch_bin2(const FastArgs& a, cudaStream_t s, int* grid_out) {
     const int grid = tiles < cap ? tiles : cap;
     if (grid_out) *grid_out = grid;
     if (grid == 0) return cudaSuccess;
-    k_bin2<W><<<grid, 2 * TR, Plan<W>::bytes(BIN), s>>>(a);
+    k_bin2<W, kBinTPR><<<grid, kBinTPR * TR, Plan<W>::bytes(BIN), s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1071,7 +1070,7 @@ cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {set_attr<W, FWD, 0>(), set_attr<W, FWD, 8>(), set_attr<W, FWD, 16>(), set_attr<W, INV, 0>(), set_attr<W, INV, 8>(),
                           set_attr<W, INV, 16>(),
-                          cudaFuncSetAttribute(k_bin2<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
+                          cudaFuncSetAttribute(k_bin2<W, kBinTPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
         if (r != cudaSuccess) e = r;
     return e;
 }
