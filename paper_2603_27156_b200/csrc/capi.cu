@@ -1372,8 +1372,8 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
 // class is launched `reps` times on the context stream between CUDA events
 // with the real step's arguments (layer 0). out[c*4 + 0..3] = ms per launch,
 // algorithmic bytes per launch, launches per training step, flops per launch.
-// Classes: 0 fused forward block, 1 backward recompute block (+dW),
-// 2 backward input-gradient block, 3 GS of the group sum.
+// Classes: 0 fused forward block, 1 backward recompute block (fast sweep: with
+// its GS epilogue), 2 backward input-gradient block (+dW), 3 GS of the group sum.
 int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
     return guarded(ctx, [&] {
         ctx->require_data();
@@ -1396,7 +1396,9 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         if (ctx->fast() && ctx->cfg.use_weight) {
             // the three fast-path block kernels (each with its hub-row pre-pass) at layer 0, block 1
             out[0] = time_it([&] { ctx->fast_block_forward(l, 1, ctx->recA, ctx->recB); });
-            out[4] = time_it([&] { ctx->fast_inverse(l, 1, ctx->recA); });
+            // INV as the backward sweep runs it for blocks 0..C-2: with the GS
+            // epilogue writing the lower layer's records (block C-1 has none)
+            out[4] = time_it([&] { ctx->fast_inverse(l, 1, ctx->recA, ctx->recB); });
             out[8] = time_it([&] { ctx->fast_input_grad(l, 1, ctx->recA); });
         }
         TileArgs fa = ctx->tile_base();
@@ -1411,7 +1413,8 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         TileArgs ra = fa;
         ra.epi = EPI_SUB; ra.gs_out = nullptr; ra.G = ctx->plane(ctx->G, 1); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
         if (!fp) out[4] = time_it([&] { ctx->run_tile(ra); });
-        out[5] = csr + n * rb + ((ctx->fast() && ctx->cfg.use_weight) ? 8 : 12) * n * w;  // fast path: dW rides on BIN
+        out[5] = fp ? csr + 2 * n * rb + 8 * n * w   // fast path: dW rides on BIN; records out
+                    : csr + n * rb + 12 * n * w;
         out[6] = L * C;
         out[7] = 4 * n * w * w;
         TileArgs ba = ctx->tile_base();
@@ -1424,7 +1427,7 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         out[11] = 2 * n * w * w;
         out[12] = time_it([&] { ctx->run_gs_groupsum(ctx->X, ctx->recB); });
         out[13] = (C - 1) * 4 * n * w + n * rb;
-        out[14] = L * (C + 1);
+        out[14] = ctx->fast_sweep() ? 2 * L : L * (C + 1);  // fast sweep: the group sums only (+ C-1 single planes once)
         out[15] = 0;
     });
 }
