@@ -150,6 +150,8 @@ struct gsrc_ctx {
     // activation arena
     Arena arena;
     float *X = nullptr, *G = nullptr, *M1 = nullptr, *M2 = nullptr, *U = nullptr, *Zh = nullptr;
+    float* Zh2 = nullptr;     // dense (transpose) hub-row aggregates: BIN's, built on the side stream
+    float* Pseg2 = nullptr;   // their segment partials
     std::vector<CUtensorMap> xmaps, gmaps;  // TMA maps of the X and G planes (fast path)
     uint8_t *recA = nullptr, *recB = nullptr, *t1 = nullptr, *t2 = nullptr, *vg = nullptr;
     std::vector<uint8_t*> rblk;  // fast backward sweep: records of block i's input (rblk[0] = recA, rblk[1] = recB)
@@ -171,6 +173,8 @@ struct gsrc_ctx {
     gsrc_optim_cfg g_step_opt{};
 
     cudaEvent_t ev[4] = {};
+    cudaStream_t side = nullptr;                 // backward sweep: dense hub pre-pass beside the INV
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t tev[3] = {};  // phase marks inside the step (Eq. 9): after forward, after backward, after optimizer
     gsrc_timing timing{};
 
@@ -183,6 +187,8 @@ struct gsrc_ctx {
         if (loss_host) cudaFreeHost(loss_host);
         for (auto& e_ : ev) if (e_) cudaEventDestroy(e_);
         for (auto& e_ : tev) if (e_) cudaEventDestroy(e_);
+        for (cudaEvent_t e_ : {fork_ev, join_ev}) if (e_) cudaEventDestroy(e_);
+        if (side) cudaStreamDestroy(side);
         if (own) cudaStreamDestroy(own);
     }
 
@@ -283,14 +289,15 @@ struct gsrc_ctx {
         return f;
     }
     float* Pseg = nullptr;  // hub segment partials (arena)
-    void run_hub(bool sparse, const FastArgs& f, bool transpose) {
+    void run_hub(bool sparse, const FastArgs& f, bool transpose, cudaStream_t s_ = nullptr) {
+        cudaStream_t st = s_ ? s_ : stream;
         const int nh = transpose ? nhub_b : nhub_f;
         if (!nh) return;
         if (sparse && !transpose) {
-            CK(launch_hub_rows(f, item_f, nitem_f, hcnt_f, Pseg, stream));
+            CK(launch_hub_rows(f, item_f, nitem_f, hcnt_f, Pseg, st));
             ++launches;
         } else if (!sparse && transpose) {
-            CK(launch_hub_dense(f, seg_b, nseg_b, hub_b, segoff_b, nhub_b, Pseg, stream));
+            CK(launch_hub_dense(f, seg_b, nseg_b, hub_b, segoff_b, nhub_b, Pseg2, st));
             launches += 2;
         } else {
             throw Fail(GSRC_ERR_CONFIG, "hub pre-pass: unsupported direction");
@@ -354,9 +361,22 @@ struct gsrc_ctx {
         for (int i = C - 1; i >= 0; --i) {
             uint8_t* rec = rblk[static_cast<size_t>(i)];
             uint8_t* own = produce && i <= C - 2 ? rblk[static_cast<size_t>(i) + 1] : nullptr;
+            // the dense hub rows of block i need only G_i (final since block
+            // i + 1's BIN): on the side stream, beside the sparse hub pass and INV
+            const bool side_hub = nhub_b > 0;
+            if (side_hub) {
+                CK(cudaEventRecord(fork_ev, stream));
+                CK(cudaStreamWaitEvent(side, fork_ev, 0));
+                FastArgs hb = fast_base(true);
+                hb.x_in = plane(G, i);
+                hb.Zh = Zh2;
+                run_hub(false, hb, true, side);
+                CK(cudaEventRecord(join_ev, side));
+            }
             if (i == 0) run_gs_groupsum(X, rec);
             fast_inverse(l, i, rec, own);
-            fast_input_grad(l, i, rec);
+            if (side_hub) CK(cudaStreamWaitEvent(stream, join_ev, 0));
+            fast_input_grad(l, i, rec, side_hub);
             reduce_block_grads(l, i);
             if (cfg.use_bias) {
                 CK(launch_colsum(plane(G, i), static_cast<int>(n), w, ld, part, &last_grid, stream));
@@ -367,10 +387,12 @@ struct gsrc_ctx {
         }
     }
     bool fast_sweep() const { return fast() && cfg.use_weight && cfg.mode == GSRC_MODE_GSRC && C >= 2; }
-    void fast_input_grad(int l, int i, const uint8_t* rec) {
+    // hub_done: the dense hub pre-pass into Zh2 was already enqueued (side stream)
+    void fast_input_grad(int l, int i, const uint8_t* rec, bool hub_done = false) {
         FastArgs b = fast_base(true);
         b.x_in = plane(G, i);
-        run_hub(false, b, true);
+        b.Zh = Zh2;
+        if (!hub_done) run_hub(false, b, true);
         b.Wm = Wb(l, i);
         b.gemm_t = 1;
         b.mrec = rec;
@@ -606,9 +628,9 @@ struct gsrc_ctx {
         total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
         if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
-        if (fast()) total += bytes_rounded(pl * sizeof(float));            // Zh (hub-row aggregates)
+        if (fast()) total += 2 * bytes_rounded(pl * sizeof(float));        // Zh, Zh2 (hub-row aggregates)
         const size_t nsegmax = static_cast<size_t>(std::max(nseg_f, nseg_b));
-        if (fast()) total += bytes_rounded(std::max<size_t>(nsegmax, 1) * ld * sizeof(float));  // Pseg
+        if (fast()) total += 2 * bytes_rounded(std::max<size_t>(nsegmax, 1) * ld * sizeof(float));  // Pseg, Pseg2
         if (alg12) total += 2 * bytes_rounded(pl * sizeof(float)) + 3 * bytes_rounded(rb) + 2 * static_cast<size_t>(cfg.layers) * bytes_rounded(rb);
         arena.plan(total);
         X = arena.lease<float>(pl * C);
@@ -627,6 +649,8 @@ struct gsrc_ctx {
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
         Zh = fast() ? arena.lease<float>(pl) : nullptr;
         Pseg = fast() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
+        Zh2 = fast() ? arena.lease<float>(pl) : nullptr;
+        Pseg2 = fast() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
         xmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         gmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         if (fast())
@@ -744,6 +768,9 @@ int gsrc_create(int device, gsrc_ctx** out) {
     ctx->stream = ctx->own;
     for (auto& e : ctx->ev) cudaEventCreate(&e);
     for (auto& e : ctx->tev) cudaEventCreate(&e);
+    if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
+    cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     if (init_kernel_attributes() != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     if (cudaMallocHost(&ctx->loss_host, sizeof(double)) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     *out = ctx;
