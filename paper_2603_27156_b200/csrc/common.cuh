@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -11,6 +12,16 @@ namespace dev {
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// Programmatic dependent launch (launch_pdl): a kernel launched with it may
+// start while its stream predecessor finishes. pdl_wait() blocks until the
+// predecessor has completed and its memory is visible — every PDL kernel calls
+// it before touching global memory that a predecessor writes or reads
+// (only parameters, the graph structure and on-chip state come before).
+// pdl_trigger() lets the successor launch once every CTA of this grid has
+// called it (or exited): persistent kernels call it on their last tile.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // GS top-k selection (ledger :121-126)
@@ -201,4 +212,21 @@ __device__ __forceinline__ void gs_select_row(const float* xrow, int w, int k, u
 }
 
 }  // namespace dev
+
+// host: launch `kern` with programmatic stream serialization (see pdl_wait)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace gsrk

@@ -405,9 +405,11 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
     const uint32_t tmem = *tslot;
     const uint32_t tlane = static_cast<uint32_t>(32 * wid) << 16;
     uint32_t ph0 = 0, ph2 = 0;
+    dev::pdl_wait();  // the prologue above touched only W and on-chip state
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR;
+        if (KIND == INV && tile_i + static_cast<int>(gridDim.x) >= n_tiles) dev::pdl_trigger();  // measured: FWD is better without
         const int row = row0 + t;
         const bool valid = row < a.n;
         // stage the residual (FWD / INV) and gradient (INV) rows
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
     const uint32_t tlane = static_cast<uint32_t>(32 * (wid & 3)) << 16;
     uint32_t ph0 = 0, ph1 = 0;
     bool dw_pending = false;
+    dev::pdl_wait();  // the prologue above touched only W and on-chip state
     if (tid == 0 && static_cast<int>(blockIdx.x) < n_tiles) {  // the first tile's mask records
         const int nr = a.n - static_cast<int>(blockIdx.x) * TR < TR ? a.n - static_cast<int>(blockIdx.x) * TR : TR;
         prefetch_l2_bulk(a.mrec + static_cast<size_t>(blockIdx.x) * TR * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
@@ -557,6 +560,7 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR, row = row0 + t;
         const bool valid = row < a.n;
+        if (tile_i + static_cast<int>(gridDim.x) >= n_tiles) dev::pdl_trigger();
         if (dw_pending) {
             mbar_wait(&bar[1], ph1);
             ph1 ^= 1u;
@@ -796,6 +800,7 @@ __global__ void __launch_bounds__(kHubChunk) k_hub_rows(FastArgs a, const int4* 
     __shared__ __align__(16) float slot[CH * PL];
     __shared__ int last;
     const int tid = threadIdx.x;
+    dev::pdl_wait();
     // work item: {row, first edge, end edge, first segment of the chunk}, {hub index, row's first partial}
     const int4 ia = __ldg(items + 2 * blockIdx.x), ib = __ldg(items + 2 * blockIdx.x + 1);
     const int r = ia.x, e0 = ia.y, e1 = ia.z, c0 = ia.w, h = ib.x;
@@ -860,6 +865,7 @@ __global__ void __launch_bounds__(256) k_hub_seg_dense(FastArgs a, const int2* _
     constexpr int CPL = W / 32;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int sgi = blockIdx.x * 8 + wid;
+    dev::pdl_wait();
     if (sgi >= nseg) return;
     const int2 se = __ldg(segs + sgi);
     const int lo = se.x, ne = se.y - se.x;
@@ -898,6 +904,7 @@ __global__ void __launch_bounds__(256) k_hub_fold(FastArgs a, const int* __restr
     constexpr int CPL = W / 32;
     const int lane = threadIdx.x & 31;
     const int h = blockIdx.x * 8 + (threadIdx.x >> 5);
+    dev::pdl_wait();
     if (h >= nhub) return;
     const int s0 = __ldg(seg_off + h), s1 = __ldg(seg_off + h + 1);
     float z[CPL];
@@ -942,6 +949,7 @@ __global__ void __launch_bounds__(TR, 3) k_gs_tma(const __grid_constant__ GsArgs
     const int nl = my_tiles * a.nplanes;  // this CTA's loads: (tile, plane) in order
     if (t == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
     __syncthreads();
+    dev::pdl_wait();
     auto issue = [&](int j) {
         const int tile_i = blockIdx.x + (j / a.nplanes) * gridDim.x, p = j % a.nplanes;
         float* dst = buf + (j & 1) * TR * W;
@@ -953,6 +961,7 @@ __global__ void __launch_bounds__(TR, 3) k_gs_tma(const __grid_constant__ GsArgs
     uint32_t ph[2] = {0u, 0u};
     float acc[W];
     for (int j = 0; j < nl; ++j) {
+        if (j + a.nplanes >= nl) dev::pdl_trigger();  // this CTA's last tile
         if (t == 0 && j + 1 < nl) issue(j + 1);  // the other buffer was released by the barrier below
         mbar_wait(&bar[j & 1], ph[j & 1]);
         ph[j & 1] ^= 1u;
@@ -1023,8 +1032,7 @@ cudaError_t launch(const FastArgs& a, cudaStream_t s, int* grid_out) {
     const int grid = tiles < cap ? tiles : cap;
     if (grid_out) *grid_out = grid;
     if (grid == 0) return cudaSuccess;
-    k_fast<W, KIND, KS><<<grid, TR, Plan<W>::bytes(KIND), s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_fast<W, KIND, KS>, dim3(grid), dim3(TR), Plan<W>::bytes(KIND), s, a);
 }
 
 template <int W, int KIND, int KS>
@@ -1061,8 +1069,7 @@ cudaError_t launch_bin2(const FastArgs& a, cudaStream_t s, int* grid_out) {
     const int grid = tiles < cap ? tiles : cap;
     if (grid_out) *grid_out = grid;
     if (grid == 0) return cudaSuccess;
-    k_bin2<W, kBinTPR><<<grid, kBinTPR * TR, Plan<W>::bytes(BIN), s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_bin2<W, kBinTPR>, dim3(grid), dim3(kBinTPR * TR), Plan<W>::bytes(BIN), s, a);
 }
 
 template <int W>
@@ -1145,20 +1152,19 @@ cudaError_t launch_gs_tma(const GsArgs& a, cudaStream_t s) {
     const int grid = tiles < cap ? tiles : cap;
     if (a.w <= 32) {
         constexpr size_t bytes = 2 * fast::TR * 32 * 4 + 64;
-        fast::k_gs_tma<32><<<grid, fast::TR, bytes, s>>>(a);
+        return launch_pdl(fast::k_gs_tma<32>, dim3(grid), dim3(fast::TR), bytes, s, a);
     } else {
         constexpr size_t bytes = 2 * fast::TR * 64 * 4 + 64;
-        fast::k_gs_tma<64><<<grid, fast::TR, bytes, s>>>(a);
+        return launch_pdl(fast::k_gs_tma<64>, dim3(grid), dim3(fast::TR), bytes, s, a);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_hub_rows(const FastArgs& a, const int4* items, int nitem, int* cnt, float* Pseg, cudaStream_t s) {
     if (nitem == 0) return cudaSuccess;
-    if (a.w <= 32) fast::k_hub_rows<32><<<nitem, kHubChunk, 0, s>>>(a, items, cnt, Pseg);
-    else if (a.w <= 64) fast::k_hub_rows<64><<<nitem, kHubChunk, 0, s>>>(a, items, cnt, Pseg);
-    else return cudaErrorInvalidValue;
-    return cudaGetLastError();
+    if (a.w <= 32) return launch_pdl(fast::k_hub_rows<32>, dim3(nitem), dim3(kHubChunk), 0, s, a, items, cnt, Pseg);
+    if (a.w <= 64) return launch_pdl(fast::k_hub_rows<64>, dim3(nitem), dim3(kHubChunk), 0, s, a, items, cnt, Pseg);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_hub_dense(const FastArgs& a, const int2* segs, int nseg, const int* rows, const int* seg_off, int nhub, float* Pseg,
@@ -1166,11 +1172,13 @@ cudaError_t launch_hub_dense(const FastArgs& a, const int2* segs, int nseg, cons
     if (nhub == 0) return cudaSuccess;
     const int gs = (nseg + 7) / 8, gf = (nhub + 7) / 8;
     if (a.w <= 32) {
-        fast::k_hub_seg_dense<32><<<gs, 256, 0, s>>>(a, segs, nseg, Pseg);
-        fast::k_hub_fold<32><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
+        cudaError_t e = launch_pdl(fast::k_hub_seg_dense<32>, dim3(gs), dim3(256), 0, s, a, segs, nseg, Pseg);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(fast::k_hub_fold<32>, dim3(gf), dim3(256), 0, s, a, rows, seg_off, nhub, static_cast<const float*>(Pseg));
     } else if (a.w <= 64) {
-        fast::k_hub_seg_dense<64><<<gs, 256, 0, s>>>(a, segs, nseg, Pseg);
-        fast::k_hub_fold<64><<<gf, 256, 0, s>>>(a, rows, seg_off, nhub, Pseg);
+        cudaError_t e = launch_pdl(fast::k_hub_seg_dense<64>, dim3(gs), dim3(256), 0, s, a, segs, nseg, Pseg);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(fast::k_hub_fold<64>, dim3(gf), dim3(256), 0, s, a, rows, seg_off, nhub, static_cast<const float*>(Pseg));
     } else {
         return cudaErrorInvalidValue;
     }
