@@ -77,8 +77,11 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__
     const int i = blockIdx.x * 32 + lane;
     const int per = (nparts + 7) / 8, p0 = c * per, p1 = min(nparts, p0 + per);
     double s = 0.0;
-    if (i < len)
+    dev::pdl_wait();
+    if (i < len) {
+#pragma unroll 8
         for (int p = p0; p < p1; ++p) s += part[static_cast<size_t>(p) * stride + i];
+    }
     red[c][lane] = s;
     __syncthreads();
     if (c == 0 && i < len) {
@@ -346,8 +349,7 @@ cudaError_t launch_gs(const GsArgs& a, cudaStream_t s) {
 
 cudaError_t launch_reduce_parts(const double* part, int nparts, int stride, int len, float* out, int accumulate, cudaStream_t s) {
     if (len <= 0) return cudaSuccess;
-    k_reduce_parts<<<blocks_for(len, 32), 256, 0, s>>>(part, nparts, stride, len, out, accumulate);
-    return cudaGetLastError();
+    return launch_pdl(k_reduce_parts, dim3(blocks_for(len, 32)), dim3(256), 0, s, static_cast<const double*>(part), nparts, stride, len, out, accumulate);
 }
 
 cudaError_t launch_sum_double(const double* in, int n, double scale, double* out, cudaStream_t s) {
