@@ -14,19 +14,26 @@
 //        parameter gradient rides on the aggregation BIN already does, so the
 //        inverse pass never reads G_i (db_i = colsum G_i: k_colsum, bias only)
 //
-// Design (one CTA = 128 threads = one 128-row tile at a time, persistent):
-//   * thread t owns tile row t end to end: it walks its CSR edges (≤ kSeg;
-//     longer "hub" rows come pre-aggregated from k_hub_* in the oracle's
-//     canonical segment order), accumulates straight into its row of the UMMA
-//     A operand in shared memory (K-major SWIZZLE_128B), scales and rounds it
-//     to TF32, reads its accumulator row back from TMEM (warp w ↔ lane
-//     quadrant w), and runs its row's epilogue and GS top-k alone — no
-//     cross-thread exchange, so the only CTA barriers are around the MMA;
-//   * the residual / gradient row tiles are staged with cp.async (LDGSTS)
-//     into swizzled shared memory while the aggregation runs;
+// Design (persistent CTAs, one 128-row tile at a time):
+//   * FWD / INV (128 threads): thread t owns tile row t end to end. It reads its
+//     row's 8 neighbour slots (Dir::ell, row-addressed), walks its ≤ kSeg
+//     edges (longer "hub" rows come pre-aggregated from k_hub_rows in the
+//     oracle's canonical segment order), accumulates straight into its row of
+//     the UMMA A operand in shared memory (K-major SWIZZLE_128B), scales it,
+//     reads its accumulator row back from TMEM (warp w ↔ lane quadrant w), adds
+//     or subtracts the residual row (a TMA tile load into the released A
+//     buffer), and runs its row's GS top-k alone (FWD: the next block's
+//     records; INV: the lower layer's records in the backward sweep);
+//   * the output tile leaves by TMA store; the next tile's residual and
+//     neighbour slots are prefetched to L2 at tile start;
+//   * BIN (256 threads): 8-lane groups gather each row of Y = Âᵀ·G_i with
+//     whole-line loads, the thread pair of a row splits the epilogue columns;
+//     the masked tile is TMA reduce-added into the destination planes;
 //   * one elected thread issues tcgen05.mma kind::tf32 (M = 128, N = W) and,
 //     for BIN, a second MN-major MMA accumulating dW = Sᵀ·Y in TMEM across all
-//     tiles of the CTA (per-CTA partials, reduced in fixed order afterwards).
+//     tiles of the CTA (per-CTA partials, reduced in fixed order afterwards);
+//   * every kernel is launched with programmatic dependent launch: the
+//     on-chip prologue overlaps the predecessor (dev::pdl_wait / pdl_trigger).
 // Arithmetic per row is the oracle's (oracle/gsr_oracle.hpp, TF32 mode):
 // canonical segmented aggregation, row scale; fp32 operands are handed to the
 // tensor core as they are, which reads them as TF32 by truncating the low 13
@@ -76,9 +83,6 @@ struct Plan {
     static constexpr size_t bytes(int kind) { return static_cast<size_t>(floats(kind) + 64) * sizeof(float); }
 };
 
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes) : "memory");
-}
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -112,23 +116,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Stage rows [row0, row0 + TR) of an n × ld plane into a swizzled smem tile
-// (columns ≥ ld zero-filled), coalesced 16 B chunks.
-template <int W, bool B32>
-__device__ __forceinline__ void stage_tile(float* dst, const float* src, int row0, int n, int ld) {
-    constexpr int CPR = W / 4;
-    for (int i = threadIdx.x; i < TR * CPR; i += TR) {
-        const int r = i / CPR, c = (i % CPR) * 4;
-        const bool ok = row0 + r < n && c < ld;
-        const float* g = ok ? src + static_cast<size_t>(row0 + r) * ld + c : src;
-        cp_async16(dst + (B32 ? zb(r, c) : zo(r, c)), g, ok ? 16 : 0);
-    }
-    cp_async_commit();
-}
-
+// K-major SWIZZLE_128B (layout type 2): LBO as given, SBO = 8-row group stride (1 KB).
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
     return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) | (64ull << 32) | (1ull << 46) |
            (2ull << 61);
