@@ -93,7 +93,8 @@ def test_fast_layer_forward_backward(ctx, oracle_tf32, C, D, k, norm, bias):
     assert gerr <= TF32_GRAD_RTOL, gerr
 
 
-@pytest.mark.parametrize("C,D,k,hubs,iso", [(4, 256, 16, (10, 60), 0), (4, 256, 16, (900, 2500), 0), (2, 64, 8, (300, 700), 37)])
+@pytest.mark.parametrize("C,D,k,hubs,iso", [(4, 256, 16, (10, 60), 0), (4, 256, 16, (900, 2500), 0), (2, 64, 8, (300, 700), 37),
+                                          (8, 256, 8, (300, 700), 0)])
 def test_fast_train_step(ctx, oracle_tf32, C, D, k, hubs, iso):
     """Whole step (encoder, L GSR-C layers, head, masked MSE, backward with
     inverse recomputation): hub rows spanning several k_hub rounds (> 1024
