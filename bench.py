@@ -15,8 +15,12 @@ mask) copied from pinned host memory and the loss read back.
 
 --impl reference times the reference CPU path: the CPU oracle
 (oracle/, a restatement of /root/reference/SPEC.md — the reference itself ships
-no compilable sources) on all host threads, on a bounded sample of the same
-workload (1 and 2 of the 80 layers at full N, extrapolated linearly in L).
+no compilable sources) on all host threads. Each timed step is a bounded sample
+of the same workload — forward + loss + backward + Adam at full N with 2 of the
+80 layers — and `ms_per_step` is what that sample took; `value` is the full
+80-layer step rate extrapolated linearly in L from the sample and a 1-layer
+calibration run (linearity in L and one real 80-layer CPU step are committed in
+profiles/r2_cpu_linearity.json, tools/cpu_linearity.py).
 """
 from __future__ import annotations
 
@@ -42,11 +46,30 @@ CONFIGS = {
     "c5": ("c5", 200, 256, 8, 8),
 }
 WORKLOAD = {
-    "c3": "1M-node / ~4M-edge synthetic circuit graph, GSR-GNN 80 layers, hidden 256, 4 groups, 25% group-sparse top-k (k=16 of 64), FP32 full-batch",
-    "c1": "10k-node / ~40k-edge synthetic circuit graph, 8 layers, hidden 64, 2 groups, k=8",
-    "c2": "100k-node synthetic circuit graph, 28 layers, hidden 128, 4 groups, k=8",
-    "c5": "10M-node power-law circuit graph, 200 layers, hidden 256, 8 groups, k=8",
+    "c3": "1M-node / ~4M-edge synthetic circuit graph, GSR-GNN 80 layers, hidden 256, 4 groups, 25% group-sparse top-k (k=16 of 64), full-batch",
+    "c1": "10k-node / ~40k-edge synthetic circuit graph, 8 layers, hidden 64, 2 groups, k=8, full-batch",
+    "c2": "100k-node synthetic circuit graph, 28 layers, hidden 128, 4 groups, k=8, full-batch",
+    "c5": "10M-node power-law circuit graph, 200 layers, hidden 256, 8 groups, k=8, full-batch",
 }
+
+
+def workload(cfg, gemm, mode="gsrc"):
+    prec = {"tf32": "FP32 storage, TF32 tensor-core block transforms (tcgen05 kind::tf32, FP32 accumulate)",
+            "fp32": "FP32-strict (block transforms as FP32 FMA chains on the CUDA cores)",
+            "cpu": "FP32 CPU oracle"}[gemm]
+    m = {"gsrc": "GSR-C", "alg12": "Alg. 1/2", "rev": "rev-baseline (RevGNN dense blocks)"}[mode]
+    return f"{WORKLOAD[cfg]}; {m}; {prec}"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 METRIC = "GSR-GNN train steps/s & peak HBM (80 layers, 1M-node graph) at 1/2/4/8 GPU"
 # Adam learning rate. SPEC.md:639's default 1e-3 diverges at 80 layers from this
 # init (CPU oracle, scratch-checked: loss 0.48 → 218 after one step); 1e-4 trains.
@@ -147,30 +170,39 @@ def build_inputs(cfg_name, rank):
     return synth.generate_synthetic(synth.config_graph(gname, seed=rank))
 
 
-def cpu_baseline(cfg_name, g, nd, mode_id, threads):
-    """Oracle (CPU restatement of the reference) on a bounded sample: the full
-    graph with 1 and 2 layers; step time extrapolated linearly in L."""
+def _oracle_sample(cfg_name, g, nd, mode_id, layers):
+    """One oracle step (fwd + loss + bwd + Adam) at full N with `layers` layers: seconds."""
     from oracle import oracle as o
     from paper_2603_27156_b200 import model
+    _, _, D, C, k = CONFIGS[cfg_name]
+    og = o.Graph(g.row_ptr, g.col_idx, norm=1)
+    net = o.Net(og, mode_id, layers, D, C, k, nd.features.shape[1], dtype=np.float32)
+    net.set_params(model.init_params(mode_id, layers, D, C, nd.features.shape[1], seed=1))
+    t0 = time.perf_counter()
+    net.loss_grads(nd.features, nd.labels, nd.train_mask)
+    p = net.params()
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    o.adam(p, net.grads(), m, v, 1, lr=LR)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg_name, g, nd, mode_id, threads, samples=1):
+    """Oracle (CPU restatement of the reference) on a bounded sample: the full
+    graph with 1 layer (calibration) and 2 layers (`samples` timed runs); the
+    80-layer step time is extrapolated linearly in L (linearity checked in
+    profiles/r2_cpu_linearity.json)."""
+    from oracle import oracle as o
     _, L, D, C, k = CONFIGS[cfg_name]
     o.set_threads(threads)
-    og = o.Graph(g.row_ptr, g.col_idx, norm=1)
-    ts = {}
-    for l in (1, 2):
-        net = o.Net(og, mode_id, l, D, C, k, nd.features.shape[1], dtype=np.float32)
-        net.set_params(model.init_params(mode_id, l, D, C, nd.features.shape[1], seed=1))
-        t0 = time.perf_counter()
-        net.loss_grads(nd.features, nd.labels, nd.train_mask)
-        p = net.params()
-        m = np.zeros_like(p)
-        v = np.zeros_like(p)
-        o.adam(p, net.grads(), m, v, 1, lr=LR)
-        ts[l] = time.perf_counter() - t0
-    per_layer = max(ts[2] - ts[1], 1e-9)
-    step = ts[1] + (L - 1) * per_layer
-    return {"value": 1.0 / step, "unit": "steps/s", "cores": threads, "kind": "port",
-            "sample": f"oracle fwd+loss+bwd+Adam at full N={g.n}, E={g.e} with L=1 ({ts[1]:.2f}s) and L=2 ({ts[2]:.2f}s); "
-                      f"step time extrapolated to L={L}: {step:.1f}s"}
+    t1 = _oracle_sample(cfg_name, g, nd, mode_id, 1)
+    t2s = [_oracle_sample(cfg_name, g, nd, mode_id, 2) for _ in range(samples)]
+    t2 = statistics.median(t2s)
+    step = t2 + (L - 2) * max(t2 - t1, 1e-9)
+    return {"value": 1.0 / step, "unit": "steps/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"oracle fwd+loss+bwd+Adam at full N={g.n}, E={g.e}: L=1 {t1:.2f}s, L=2 {t2:.2f}s; "
+                      f"{L}-layer step extrapolated linearly in L: {step:.1f}s",
+            "sample_s": t2, "calibration_s": t1, "extrapolated_step_s": step}
 
 
 def host_threads():
@@ -181,28 +213,36 @@ def host_threads():
 
 
 def run_reference(args):
+    """Reference arm: the CPU oracle on the host cores (rank 0 only). Each step
+    is a bounded sample (full N, 2 layers); value = the extrapolated full-depth
+    step rate, ms_per_step = the sample's measured time."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle import oracle as o
     _, L, D, C, k = CONFIGS[args.config]
     mode_id = {"alg12": 0, "gsrc": 1, "rev": 2}[args.mode]
     g, nd = build_inputs(args.config, 0)
     th = host_threads()
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, g, nd, mode_id, th)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    v = statistics.median(vals)
+    o.set_threads(th)
+    t1 = _oracle_sample(args.config, g, nd, mode_id, 1)   # calibration (untimed)
+    for _ in range(args.warmup):
+        _oracle_sample(args.config, g, nd, mode_id, 2)
+    t2s = [_oracle_sample(args.config, g, nd, mode_id, 2) for _ in range(args.steps)]
+    t2 = statistics.median(t2s)
+    step_s = t2 + (L - 2) * max(t2 - t1, 1e-9)
+    v = 1.0 / step_s
+    sample = (f"CPU oracle (restatement of SPEC.md; the reference ships no compilable sources), {th} threads on {cpu_model()}: "
+              f"each timed step = fwd+loss+bwd+Adam at full N={g.n} with L=2 (median {t2:.2f}s); L=1 calibration {t1:.2f}s; "
+              f"the {L}-layer step extrapolated linearly in L = {step_s:.1f}s (profiles/r2_cpu_linearity.json)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t2, "ms_per_workload_step_extrapolated": 1000.0 * step_s,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded generate_synthetic, SPEC.md:186-194)",
-        "config": {"workload": WORKLOAD[args.config], "n_nodes": g.n, "n_edges": g.e, "layers": L, "hidden": D, "groups": C, "k": k,
-                   "mode": args.mode},
-        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": th, "kind": "port",
-                         "sample": "CPU oracle (restatement of SPEC.md; reference ships no compilable sources) at full N with "
-                                   "L=1 and L=2, each step extrapolated linearly to L=%d" % L},
+        "config": {"workload": workload(args.config, "cpu", args.mode), "n_nodes": g.n, "n_edges": g.e, "layers": L, "hidden": D,
+                   "groups": C, "k": k, "mode": args.mode, "sample_layers": 2},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": th, "kind": "port", "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -225,17 +265,17 @@ def run_ours(args):
     mode_id = {"alg12": MODE_ALG12, "gsrc": MODE_GSRC, "rev": MODE_REV}[args.mode]
     d_in = 8
     g, nd = build_inputs(args.config, rank)
-    stream = torch.cuda.current_stream()
     free0, total = torch.cuda.mem_get_info()
     ctx = Context(local)
-    ctx.set_stream(stream.cuda_stream)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr())  # the context's stream: the timing events go on it
     ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
     ctx.model_init(mode_id, L, D, C, k, d_in, gemm=GEMM_TF32 if args.gemm == "tf32" else GEMM_FP32)
     p0 = model.init_params(mode_id, L, D, C, d_in, seed=1)
     ctx.set_params(p0)
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
     ctx.set_graph_capture(not args.no_graph)
-    step = DataParallelStep(ctx, lr=LR)   # world 1: fused train_step; world > 1: fwd/bwd → NCCL all-reduce(avg) → Adam
+    # world 1: fused train_step; world > 1: the library's NCCL communicator, fwd/bwd → all-reduce(avg) → Adam on one stream
+    step = DataParallelStep(ctx, lr=LR)
 
     losses = [step() for _ in range(args.warmup)]
     ctx.high_water_reset()
@@ -320,9 +360,10 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.gemm == "fp32" else "f32 (tf32 tensor-core transform)",
             "data": "synthetic (seeded generate_synthetic SPEC.md:186-194; random-init weights)",
-            "config": {"workload": WORKLOAD[args.config], "n_nodes": g.n, "n_edges": g.e, "layers": L, "hidden": D, "groups": C, "k": k,
+            "config": {"workload": workload(args.config, args.gemm, args.mode), "n_nodes": g.n, "n_edges": g.e, "layers": L, "hidden": D, "groups": C, "k": k,
                        "d_in": d_in, "mode": args.mode, "optimizer": f"adam lr={LR}", "gemm": "tcgen05 kind::tf32 (fp32 accumulate)" if args.gemm == "tf32" else "fp32-strict (CUDA cores)", "parallelism": f"dp{world}",
                        "subgraph_per_rank": "seed = rank", "l2": "inputs larger than L2 (activations 1 GB/plane set)",
+                       "dp": "native NCCL all-reduce in the library" if world > 1 else "single rank",
                        "cuda_graph": not args.no_graph},
             "edges_layers_per_s": value * g.e * L,
             "phases_ms_last_step": phases,

@@ -76,7 +76,11 @@ typedef struct { double t_forward, t_backward, t_copy, t_optimizer, t_total; } g
 int gsrc_create(int device, gsrc_ctx** out);
 void gsrc_destroy(gsrc_ctx* ctx);
 const char* gsrc_last_error(gsrc_ctx* ctx);
-int gsrc_set_stream(gsrc_ctx* ctx, void* cuda_stream);     /* NULL = context-owned stream */
+/* Bind the context to a caller's cudaStream_t. NULL selects the context-owned
+   non-blocking stream (the default) — NOT the legacy default stream: a caller
+   that must order its own work with the context's uses gsrc_get_stream. */
+int gsrc_set_stream(gsrc_ctx* ctx, void* cuda_stream);
+int gsrc_get_stream(gsrc_ctx* ctx, void** cuda_stream_out);  /* the stream every call enqueues on */
 int gsrc_synchronize(gsrc_ctx* ctx);
 int gsrc_version(char* buf, size_t len);                    /* kArtifactVersion common.hpp:9 */
 
@@ -110,9 +114,35 @@ int gsrc_last_timing(gsrc_ctx* ctx, gsrc_timing* out);
 int gsrc_mem_stats(gsrc_ctx* ctx, gsrc_mem_report* out);                  /* Arena::stats SPEC.md:486-490 */
 int gsrc_high_water_reset(gsrc_ctx* ctx);
 int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out);                    /* kernels enqueued since create */
-/* Live per-kernel timing for the roofline report: out[16] = 4 kernel classes ×
-   {ms per launch, algorithmic bytes per launch, launches per step, flops per launch}. */
+/* Live per-kernel timing for the roofline report. out must hold 16 + 3·C
+   doubles: out[0..15] = 4 kernel classes × {ms per launch (mean over the C
+   blocks), algorithmic bytes per launch, launches per step, flops per launch},
+   then out[16 + c·C + i] = ms per launch of block i for classes c = 0..2.
+   The activation arena is snapshotted and restored: no device state changes. */
 int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out);
+
+/* Optimizer state for exact resume (the GSRP checkpoint holds parameters
+   only): Adam first/second moments and the step count. */
+int gsrc_optim_state_get(gsrc_ctx* ctx, float* m, float* v, int64_t* step, int64_t n);
+int gsrc_optim_state_set(gsrc_ctx* ctx, const float* m, const float* v, int64_t step, int64_t n);
+
+/* ---- data parallelism (one process or thread per GPU) ----------
+   Each rank trains on its own subgraph; gsrc_train_step then averages the flat
+   gradient buffer over the ranks with one NCCL all-reduce on the context stream,
+   between backward and optimizer. NCCL is loaded at run time (libnccl.so.2);
+   without it these return GSRC_ERR_RESOURCE. */
+int gsrc_comm_unique_id(void* out, size_t len);                         /* rank 0: len ≥ 128 (ncclUniqueId) */
+int gsrc_comm_init(gsrc_ctx* ctx, const void* unique_id, int nranks, int rank);
+int gsrc_comm_allreduce_grads(gsrc_ctx* ctx);                           /* for the split forward_backward / optimizer_step path */
+int gsrc_comm_destroy(gsrc_ctx* ctx);
+
+/* ---- reconstruction diagnostics (GSRC) ------------------------------------------
+   With diagnostics on, the forward stores the GS mask (index bytes) of every
+   row_stride-th row for each (layer, block), and the backward counts the sampled
+   rows whose mask recomputed from the reconstructed activations differs.
+   flips must hold layers × groups counts (layer-major). */
+int gsrc_diag_masks(gsrc_ctx* ctx, int enable, int row_stride);
+int gsrc_diag_mask_flips(gsrc_ctx* ctx, int64_t* flips, int64_t* sampled_rows);
 
 /* ---- layer-level entry points (device activation = gsrc_activation_*) ----- */
 int gsrc_layer_forward(gsrc_ctx* ctx, int layer);    /* gsr_forward_layer SPEC.md:386 / rev_forward_layer :316 */

@@ -70,6 +70,8 @@ EXPORTS = [
     "gsrc_gradient_set", "gsrc_set_graph_capture", "gsrc_last_timing", "gsrc_mem_stats", "gsrc_high_water_reset",
     "gsrc_kernel_launches", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
     "gsrc_set_op_precision", "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
+    "gsrc_get_stream", "gsrc_optim_state_get", "gsrc_optim_state_set", "gsrc_comm_unique_id", "gsrc_comm_init",
+    "gsrc_comm_allreduce_grads", "gsrc_comm_destroy", "gsrc_diag_masks", "gsrc_diag_mask_flips",
 ]
 
 _lib = None
@@ -118,6 +120,15 @@ def lib():
         L.gsrc_op_dense_block.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp]
         L.gsrc_op_block_backward.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
         L.gsrc_version.argtypes = [C.c_char_p, C.c_size_t]
+        L.gsrc_get_stream.argtypes = [vp, C.POINTER(vp)]
+        L.gsrc_optim_state_get.argtypes = [vp, vp, vp, C.POINTER(i64), i64]
+        L.gsrc_optim_state_set.argtypes = [vp, vp, vp, i64, i64]
+        L.gsrc_comm_unique_id.argtypes = [vp, C.c_size_t]
+        L.gsrc_comm_init.argtypes = [vp, vp, i32, i32]
+        L.gsrc_comm_allreduce_grads.argtypes = [vp]
+        L.gsrc_comm_destroy.argtypes = [vp]
+        L.gsrc_diag_masks.argtypes = [vp, i32, i32]
+        L.gsrc_diag_mask_flips.argtypes = [vp, vp, C.POINTER(i64)]
         _lib = L
     return _lib
 
@@ -168,7 +179,19 @@ class Context:
 
     # ---- setup ---------------------------------------------------------------
     def set_stream(self, stream_ptr: int | None):
-        self._chk(lib().gsrc_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+        """Bind to a caller's stream; None = the context-owned stream. Handle 0
+        (the legacy default stream) is rejected: the C-ABI reads NULL as "own
+        stream", which would silently lose the ordering the caller asked for."""
+        if stream_ptr == 0:
+            raise ConfigError("set_stream(0): the legacy default stream cannot be bound; use a torch.cuda.Stream "
+                              "or None (context-owned stream, see stream_ptr())")
+        self._chk(lib().gsrc_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t every call enqueues on (wrap with torch.cuda.ExternalStream to order torch work with it)."""
+        s = C.c_void_p()
+        self._chk(lib().gsrc_get_stream(self.h, C.byref(s)))
+        return s.value or 0
 
     def graph_upload(self, row_ptr, col_idx, norm=NORM_ROW_MEAN):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -300,13 +323,58 @@ class Context:
     KERNEL_CLASSES = ("fused_block_fwd", "block_bwd_recompute", "block_bwd_input", "gs_groupsum")
 
     def profile_kernels(self, reps=20):
-        out = np.zeros(16, np.float64)
+        """Live CUDA-event timing of each kernel class over all C blocks (device state preserved)."""
+        Cg = self.cfg["groups"]
+        out = np.zeros(16 + 3 * Cg, np.float64)
         self._chk(lib().gsrc_profile_kernels(self.h, int(reps), _p(out)))
         res = {}
         for c, name in enumerate(self.KERNEL_CLASSES):
             ms, byts, per_step, flops = out[4 * c:4 * c + 4]
             res[name] = dict(ms=float(ms), bytes=float(byts), launches_per_step=float(per_step), flops=float(flops))
+            if c < 3:
+                res[name]["ms_per_block"] = [float(x) for x in out[16 + c * Cg:16 + (c + 1) * Cg]]
         return res
+
+    # ---- optimizer state / data parallelism / diagnostics -------------------------
+    def optim_state(self):
+        m = np.zeros(self.P, np.float32)
+        v = np.zeros(self.P, np.float32)
+        t = C.c_int64()
+        self._chk(lib().gsrc_optim_state_get(self.h, _p(m), _p(v), C.byref(t), self.P))
+        return m, v, t.value
+
+    def set_optim_state(self, m, v, step):
+        m, v = _f32(m), _f32(v)
+        self._chk(lib().gsrc_optim_state_set(self.h, _p(m), _p(v), int(step), self.P))
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = lib().gsrc_comm_unique_id(buf, 128)
+        if st != 0:
+            raise _ERRS.get(st, GsrError)("gsrc_comm_unique_id failed (NCCL unavailable?)")
+        return buf.raw
+
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._chk(lib().gsrc_comm_init(self.h, buf, int(nranks), int(rank)))
+
+    def comm_allreduce_grads(self):
+        self._chk(lib().gsrc_comm_allreduce_grads(self.h))
+
+    def comm_destroy(self):
+        self._chk(lib().gsrc_comm_destroy(self.h))
+
+    def diag_masks(self, enable=True, row_stride=1):
+        self._chk(lib().gsrc_diag_masks(self.h, int(enable), int(row_stride)))
+
+    def mask_flips(self):
+        """(layers × groups) counts of sampled rows whose backward-recomputed GS mask differs from the forward's, and the sample size."""
+        L, Cg = self.cfg["layers"], self.cfg["groups"]
+        f = np.zeros(L * Cg, np.int64)
+        rows = C.c_int64()
+        self._chk(lib().gsrc_diag_mask_flips(self.h, _p(f), C.byref(rows)))
+        return f.reshape(L, Cg), rows.value
 
     # ---- op-level parity entry points (SPEC op names) ----------------------------
     def set_op_precision(self, gemm):

@@ -16,6 +16,9 @@
 #include "../../include/gsr_cuda.h"
 #include "kernels.cuh"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -106,6 +109,44 @@ struct DevBuf {  // scratch for op-level parity entry points
     template <typename T> T* as() { return static_cast<T*>(p); }
 };
 
+// NCCL, resolved at run time (dlopen) so the library loads on hosts without
+// it; inside a torch process the already-loaded libnccl.so.2 is reused. Only
+// the data-parallel entry points (gsrc_comm_*) need it (one
+// gradient all-reduce per step).
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    std::string why;
+    bool ok() const { return get_unique_id && comm_init_rank && all_reduce && comm_destroy && error_string; }
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { a.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror(); return a; }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!a.ok()) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+const NcclApi& nccl_or_throw() {
+    const NcclApi& a = nccl_api();
+    if (!a.ok()) throw Fail(GSRC_ERR_RESOURCE, "NCCL unavailable: " + a.why);
+    return a;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Fail(GSRC_ERR_RESOURCE, std::string(what) + ": " + nccl_api().error_string(r));
+}
+
 }  // namespace
 
 struct gsrc_ctx {
@@ -175,8 +216,21 @@ struct gsrc_ctx {
     cudaEvent_t ev[4] = {};
     cudaStream_t side = nullptr;                 // backward sweep: dense hub pre-pass beside the INV
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    cudaEvent_t tev[3] = {};  // phase marks inside the step (Eq. 9): after forward, after backward, after optimizer
+    cudaEvent_t tev[4] = {};  // phase marks inside the step (Eq. 9): after forward, after backward, after optimizer, after the all-reduce
     gsrc_timing timing{};
+
+    // data parallelism: one NCCL communicator, the gradient all-reduce (average)
+    // between backward and optimizer on the context stream (gsrc_comm_init)
+    ncclComm_t comm = nullptr;
+    int comm_ranks = 1, comm_rank = 0;
+
+    // mask-flip diagnostic (gsrc_diag_masks): forward GS index bytes of every
+    // stride-th row per (layer, block), compared with the backward's recomputed masks
+    bool diag = false;
+    int diag_stride = 1;
+    int64_t diag_rows = 0;
+    uint4* diag_store = nullptr;
+    unsigned long long* diag_cnt = nullptr;
 
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
@@ -188,6 +242,9 @@ struct gsrc_ctx {
         for (auto& e_ : ev) if (e_) cudaEventDestroy(e_);
         for (auto& e_ : tev) if (e_) cudaEventDestroy(e_);
         for (cudaEvent_t e_ : {fork_ev, join_ev}) if (e_) cudaEventDestroy(e_);
+        if (diag_store) cudaFree(diag_store);
+        if (diag_cnt) cudaFree(diag_cnt);
+        if (comm) nccl_api().comm_destroy(comm);
         if (side) cudaStreamDestroy(side);
         if (own) cudaStreamDestroy(own);
     }
@@ -272,6 +329,16 @@ struct gsrc_ctx {
         float* dst = grads + off_block(l, i);
         if (cfg.use_weight) CK(launch_reduce_parts(part, last_grid, plen, plen, dst, 1, stream));
         else CK(launch_reduce_parts(part + static_cast<size_t>(w) * w, last_grid, plen, w, dst + static_cast<size_t>(w) * w, 1, stream));
+        ++launches;
+    }
+
+    // mask-flip diagnostic: mode 0 stores the forward masks of block i of layer
+    // l, mode 1 counts the sampled rows whose backward recompute differs
+    void diag_rec(int l, int i, const uint8_t* rec, int mode) {
+        if (!diag || cfg.mode != GSRC_MODE_GSRC) return;
+        const size_t slot = static_cast<size_t>(l) * C + static_cast<size_t>(i);
+        CK(launch_diag_masks(rec, static_cast<int>(n), diag_stride, rec_bytes(k), diag_store + slot * static_cast<size_t>(diag_rows), mode,
+                             diag_cnt + slot, stream));
         ++launches;
     }
 
@@ -374,6 +441,7 @@ struct gsrc_ctx {
                 CK(cudaEventRecord(join_ev, side));
             }
             if (i == 0) run_gs_groupsum(X, rec);
+            diag_rec(l, i, rec, 1);
             fast_inverse(l, i, rec, own);
             if (side_hub) CK(cudaStreamWaitEvent(stream, join_ev, 0));
             fast_input_grad(l, i, rec, side_hub);
@@ -415,12 +483,14 @@ struct gsrc_ctx {
         else run_sum_planes(X, U);
         if (fast() && cfg.use_weight) {
             for (int i = 0; i < C; ++i) {
+                diag_rec(l, i, cur, 0);
                 fast_block_forward(l, i, cur, i + 1 < C ? nxt : nullptr);
                 std::swap(cur, nxt);
             }
             return;
         }
         for (int i = 0; i < C; ++i) {
+            if (sparse) diag_rec(l, i, cur, 0);
             TileArgs a = tile_base();
             a.dir = fwd();
             if (sparse) {
@@ -449,6 +519,7 @@ struct gsrc_ctx {
         if (sparse) {
             if (i > 0) run_gs({plane(X, i - 1)}, recA);
             else run_gs_groupsum(X, recA);
+            if (with_grads) diag_rec(l, i, recA, 1);
         } else {
             if (i > 0) u = plane(X, i - 1);
             else { run_sum_planes(X, U); u = U; }
@@ -556,6 +627,7 @@ struct gsrc_ctx {
     void layer_backward(int l) { if (cfg.mode == GSRC_MODE_ALG12) alg12_layer_backward(l); else rev_layer_backward(l); }
 
     void enqueue_forward() {
+        if (diag) CK(cudaMemsetAsync(diag_cnt, 0, sizeof(unsigned long long) * static_cast<size_t>(cfg.layers) * C, stream));
         CK(launch_encoder(X0, static_cast<int>(n), cfg.d_in, params, params + static_cast<size_t>(cfg.d_in) * cfg.hidden, cfg.hidden,
                           C, w, ld, X, stream));
         ++launches;
@@ -585,6 +657,13 @@ struct gsrc_ctx {
         ++launches;
     }
     void enqueue_zero_grads() { CK(cudaMemsetAsync(grads, 0, sizeof(float) * P, stream)); }
+    // one in-place NCCL all-reduce (average) of the flat gradient buffer on the
+    // context stream: ordered after the backward and before the optimizer by
+    // the stream itself
+    void enqueue_allreduce() {
+        if (!comm) return;  // a 1-rank communicator still runs the call (AVG over one rank is the identity)
+        nccl_check(nccl_api().all_reduce(grads, grads, static_cast<size_t>(P), ncclFloat32, ncclAvg, comm, stream), "ncclAllReduce");
+    }
     void enqueue_optimizer(const gsrc_optim_cfg& o) {
         if (o.optimizer == 0) {
             CK(launch_adam_prep(d_step, static_cast<double>(o.beta1), static_cast<double>(o.beta2), bc, stream));
@@ -917,7 +996,12 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
         ctx->e = e;
         ctx->norm = norm;
         ctx->drop_graphs();
-        if (resize) ctx->data = false;
+        if (resize) {
+            ctx->data = false;
+            if (ctx->diag_store) { cudaFree(ctx->diag_store); ctx->diag_store = nullptr; }
+            if (ctx->diag_cnt) { cudaFree(ctx->diag_cnt); ctx->diag_cnt = nullptr; }
+            ctx->diag = false;
+        }
         if (ctx->model) ctx->plan_arena();  // node count / hub segments changed: re-plan activations
     });
 }
@@ -960,6 +1044,9 @@ int gsrc_model_init(gsrc_ctx* ctx, const gsrc_model_cfg* cfg) {
         CK(cudaMemset(ctx->opt_v, 0, sizeof(float) * ctx->P));
         CK(cudaMemset(ctx->d_step, 0, sizeof(long long)));
         CK(cudaDeviceSynchronize());
+        if (ctx->diag_store) { cudaFree(ctx->diag_store); ctx->diag_store = nullptr; }
+        if (ctx->diag_cnt) { cudaFree(ctx->diag_cnt); ctx->diag_cnt = nullptr; }
+        ctx->diag = false;
         ctx->model = true;
         ctx->drop_graphs();
         ctx->plan_arena();
@@ -1074,7 +1161,8 @@ static gsrc_timing phase_timing(gsrc_ctx* ctx, bool with_opt) {
     cudaEventElapsedTime(&t_all, ctx->ev[0], ctx->ev[1]);
     cudaEventElapsedTime(&t_f, ctx->ev[0], ctx->tev[0]);
     cudaEventElapsedTime(&t_b, ctx->tev[0], ctx->tev[1]);
-    if (with_opt) cudaEventElapsedTime(&t_o, ctx->tev[1], ctx->tev[2]);
+    // the gradient all-reduce (tev[1] → tev[3]) and the loss read-back count as "copy"
+    if (with_opt) cudaEventElapsedTime(&t_o, ctx->tev[3], ctx->tev[2]);
     const float t_c = t_all - t_f - t_b - t_o;
     return gsrc_timing{t_f * 1e-3, t_b * 1e-3, (t_c > 0.f ? t_c : 0.f) * 1e-3, t_o * 1e-3, t_all * 1e-3};
 }
@@ -1124,6 +1212,8 @@ int gsrc_train_step(gsrc_ctx* ctx, const gsrc_optim_cfg* opt, double* loss_out) 
         CK(cudaEventRecord(ctx->tev[0], ctx->stream));
         run_maybe_graph(ctx, ctx->g_bwd, ctx->g_bwd_launches, [&] { ctx->enqueue_backward(); });
         CK(cudaEventRecord(ctx->tev[1], ctx->stream));
+        ctx->enqueue_allreduce();  // data parallel: average the gradients over the ranks (no-op without a communicator)
+        CK(cudaEventRecord(ctx->tev[3], ctx->stream));
         run_maybe_graph(ctx, ctx->g_opt, ctx->g_opt_launches, [&] { ctx->enqueue_optimizer(*opt); });
         CK(cudaEventRecord(ctx->tev[2], ctx->stream));
         CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1396,11 +1486,15 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
 }
 
 // Live per-kernel timing for the roofline report (bench.py): each GSR-C kernel
-// class is launched `reps` times on the context stream between CUDA events
-// with the real step's arguments (layer 0). out[c*4 + 0..3] = ms per launch,
-// algorithmic bytes per launch, launches per training step, flops per launch.
-// Classes: 0 fused forward block, 1 backward recompute block (fast sweep: with
-// its GS epilogue), 2 backward input-gradient block (+dW), 3 GS of the group sum.
+// class is launched `reps` times per block on the context stream between CUDA
+// events with the real step's arguments (layer 0, every block i = 0..C-1).
+// out[c*4 + 0..3] = ms per launch (mean over the blocks), algorithmic bytes per
+// launch, launches per training step, flops per launch; out[16 + c*C + i] = ms
+// per launch of block i (classes 0..2). Classes: 0 fused forward block, 1
+// backward recompute block (fast sweep: with its GS epilogue for blocks
+// 0..C-2), 2 backward input-gradient block (+dW; block 0 adds into C-1
+// planes), 3 GS of the group sum. The activation arena is snapshotted first and
+// restored afterwards, so the call leaves every device buffer as it found it.
 int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
     return guarded(ctx, [&] {
         ctx->require_data();
@@ -1408,7 +1502,25 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         if (reps < 1) cfg_err("profile: reps < 1");
         const double n = static_cast<double>(ctx->n), e = static_cast<double>(ctx->e), w = ctx->w, k = ctx->k, L = ctx->cfg.layers, C = ctx->C;
         const double rb = rec_bytes(ctx->k), csr = 4.0 * (n + 1) + 4.0 * e;
-        const int l = 0;
+        const int l = 0, nC = ctx->C;
+        // snapshot of the arena (activations, gradients, records, partials)
+        void* snap = nullptr;
+        const size_t used = ctx->arena.used;
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (cudaMalloc(&snap, used) != cudaSuccess) {
+            cudaGetLastError();
+            throw Fail(GSRC_ERR_RESOURCE, "profile: no device memory for the arena snapshot (" + std::to_string(used) + " bytes)");
+        }
+        struct Restore {
+            gsrc_ctx* c; void* p; size_t b;
+            ~Restore() {
+                cudaMemcpyAsync(c->arena.base, p, b, cudaMemcpyDeviceToDevice, c->stream);
+                cudaStreamSynchronize(c->stream);
+                cudaFree(p);
+            }
+        } restore{ctx, snap, used};
+        CK(cudaMemcpyAsync(snap, ctx->arena.base, used, cudaMemcpyDeviceToDevice, ctx->stream));
+        for (int q = 0; q < 16 + 3 * nC; ++q) out[q] = 0.0;
         ctx->run_gs({ctx->plane(ctx->X, 0)}, ctx->recA);
         auto time_it = [&](const std::function<void()>& f) {
             f();  // warm
@@ -1420,42 +1532,179 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
             CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
             return static_cast<double>(ms) / reps;
         };
-        if (ctx->fast() && ctx->cfg.use_weight) {
-            // the three fast-path block kernels (each with its hub-row pre-pass) at layer 0, block 1
-            out[0] = time_it([&] { ctx->fast_block_forward(l, 1, ctx->recA, ctx->recB); });
-            // INV as the backward sweep runs it for blocks 0..C-2: with the GS
-            // epilogue writing the lower layer's records (block C-1 has none)
-            out[4] = time_it([&] { ctx->fast_inverse(l, 1, ctx->recA, ctx->recB); });
-            out[8] = time_it([&] { ctx->fast_input_grad(l, 1, ctx->recA); });
-        }
-        TileArgs fa = ctx->tile_base();
-        fa.agg = AGG_SPARSE; fa.dir = ctx->fwd(); fa.rec_in = ctx->recA; fa.k_in = ctx->k;
-        fa.gemm = ctx->cfg.use_weight ? GEMM_W : GEMM_NONE; fa.Wm = ctx->Wb(l, 1); fa.bias = ctx->Bb(l, 1);
-        fa.epi = EPI_ADD; fa.R = ctx->plane(ctx->X, 1); fa.out = ctx->plane(ctx->X, 1); fa.gs_out = ctx->recB; fa.k_gs = ctx->k;
+        auto per_block = [&](int cls, const std::function<void(int)>& f) {
+            double sum = 0.0;
+            for (int i = 0; i < nC; ++i) {
+                const double ms = time_it([&] { f(i); });
+                out[16 + cls * nC + i] = ms;
+                sum += ms;
+            }
+            out[cls * 4] = sum / nC;
+        };
         const bool fp = ctx->fast() && ctx->cfg.use_weight;
-        if (!fp) out[0] = time_it([&] { ctx->run_tile(fa); });
+        if (fp) {
+            // the three fast-path block kernels, each with its hub-row pre-pass
+            per_block(0, [&](int i) { ctx->fast_block_forward(l, i, ctx->recA, i + 1 < nC ? ctx->recB : nullptr); });
+            // INV as the backward sweep runs it: blocks 0..C-2 write the lower layer's records
+            per_block(1, [&](int i) { ctx->fast_inverse(l, i, ctx->recA, i <= nC - 2 ? ctx->recB : nullptr); });
+            per_block(2, [&](int i) { ctx->fast_input_grad(l, i, ctx->recA); });
+        } else {
+            per_block(0, [&](int i) {
+                TileArgs fa = ctx->tile_base();
+                fa.agg = AGG_SPARSE; fa.dir = ctx->fwd(); fa.rec_in = ctx->recA; fa.k_in = ctx->k;
+                fa.gemm = ctx->cfg.use_weight ? GEMM_W : GEMM_NONE; fa.Wm = ctx->Wb(l, i); fa.bias = ctx->Bb(l, i);
+                fa.epi = EPI_ADD; fa.R = ctx->plane(ctx->X, i); fa.out = ctx->plane(ctx->X, i);
+                if (i + 1 < nC) { fa.gs_out = ctx->recB; fa.k_gs = ctx->k; }
+                ctx->run_tile(fa);
+            });
+            per_block(1, [&](int i) {
+                TileArgs ra = ctx->tile_base();
+                ra.agg = AGG_SPARSE; ra.dir = ctx->fwd(); ra.rec_in = ctx->recA; ra.k_in = ctx->k;
+                ra.gemm = ctx->cfg.use_weight ? GEMM_W : GEMM_NONE; ra.Wm = ctx->Wb(l, i); ra.bias = ctx->Bb(l, i);
+                ra.epi = EPI_SUB; ra.R = ctx->plane(ctx->X, i); ra.out = ctx->plane(ctx->X, i);
+                ra.G = ctx->plane(ctx->G, i); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
+                ctx->run_tile(ra);
+            });
+            per_block(2, [&](int i) {
+                TileArgs ba = ctx->tile_base();
+                ba.agg = AGG_DENSE; ba.dir = ctx->bwd(); ba.x_in = ctx->plane(ctx->G, i);
+                ba.gemm = ctx->cfg.use_weight ? GEMM_WT : GEMM_NONE; ba.Wm = ctx->Wb(l, i);
+                ba.epi = EPI_MASKED_ADD; ba.rrec = ctx->recA; ba.k_r = ctx->k;
+                if (i > 0) { ba.dst[0] = ctx->plane(ctx->G, i - 1); ba.ndst = 1; }
+                else { for (int p = 1; p < nC; ++p) ba.dst[p - 1] = ctx->plane(ctx->G, p); ba.ndst = nC - 1; }
+                ctx->run_tile(ba);
+            });
+        }
+        // algorithmic bytes per launch; BIN's block 0 updates C-1 planes
         out[1] = csr + 2 * n * rb + 8 * n * w;
         out[2] = L * C;
         out[3] = 2 * n * w * w;
-        TileArgs ra = fa;
-        ra.epi = EPI_SUB; ra.gs_out = nullptr; ra.G = ctx->plane(ctx->G, 1); ra.want_db = ctx->cfg.use_bias; ra.part = ctx->part;
-        if (!fp) out[4] = time_it([&] { ctx->run_tile(ra); });
         out[5] = fp ? csr + 2 * n * rb + 8 * n * w   // fast path: dW rides on BIN; records out
                     : csr + n * rb + 12 * n * w;
         out[6] = L * C;
         out[7] = 4 * n * w * w;
-        TileArgs ba = ctx->tile_base();
-        ba.agg = AGG_DENSE; ba.dir = ctx->bwd(); ba.x_in = ctx->plane(ctx->G, 1);
-        ba.gemm = ctx->cfg.use_weight ? GEMM_WT : GEMM_NONE; ba.Wm = ctx->Wb(l, 1);
-        ba.epi = EPI_MASKED_ADD; ba.rrec = ctx->recA; ba.k_r = ctx->k; ba.dst[0] = ctx->plane(ctx->G, 0); ba.ndst = 1;
-        if (!fp) out[8] = time_it([&] { ctx->run_tile(ba); });
-        out[9] = csr + 4 * n * w + n * rb + 8 * n * k;
+        out[9] = csr + 4 * n * w + n * rb + 8 * n * k * (1.0 + (C - 2) / C);  // block 0 writes C-1 planes: mean over blocks
         out[10] = L * C;
         out[11] = 2 * n * w * w;
         out[12] = time_it([&] { ctx->run_gs_groupsum(ctx->X, ctx->recB); });
         out[13] = (C - 1) * 4 * n * w + n * rb;
         out[14] = ctx->fast_sweep() ? 2 * L : L * (C + 1);  // fast sweep: the group sums only (+ C-1 single planes once)
         out[15] = 0;
+    });
+}
+
+int gsrc_get_stream(gsrc_ctx* ctx, void** out) {
+    return guarded(ctx, [&] {
+        if (!out) cfg_err("get_stream: null out");
+        *out = static_cast<void*>(ctx->stream);
+    });
+}
+
+// ---- optimizer state (exact resume: Adam m, v and the step count) -------------
+int gsrc_optim_state_get(gsrc_ctx* ctx, float* m, float* v, int64_t* step, int64_t n) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (n != ctx->P) cfg_err("optim_state_get: expected " + std::to_string(ctx->P) + " values");
+        long long t = 0;
+        if (m) CK(cudaMemcpyAsync(m, ctx->opt_m, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (v) CK(cudaMemcpyAsync(v, ctx->opt_v, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&t, ctx->d_step, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (step) *step = t;
+    });
+}
+
+int gsrc_optim_state_set(gsrc_ctx* ctx, const float* m, const float* v, int64_t step, int64_t n) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (n != ctx->P) cfg_err("optim_state_set: expected " + std::to_string(ctx->P) + " values");
+        if (step < 0) cfg_err("optim_state_set: step < 0");
+        const long long t = step;
+        if (m) CK(cudaMemcpyAsync(ctx->opt_m, m, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (v) CK(cudaMemcpyAsync(ctx->opt_v, v, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->d_step, &t, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- data parallelism (SURVEY.md §8b "DP", §8e) --------------------------------
+int gsrc_comm_unique_id(void* out, size_t len) {
+    if (!out || len < sizeof(ncclUniqueId)) return GSRC_ERR_CONFIG;
+    const NcclApi& a = nccl_api();
+    if (!a.ok()) return GSRC_ERR_RESOURCE;
+    ncclUniqueId id;
+    if (a.get_unique_id(&id) != ncclSuccess) return GSRC_ERR_RESOURCE;
+    std::memcpy(out, &id, sizeof id);
+    return GSRC_OK;
+}
+
+int gsrc_comm_init(gsrc_ctx* ctx, const void* unique_id, int nranks, int rank) {
+    return guarded(ctx, [&] {
+        if (!unique_id) cfg_err("comm_init: null unique id");
+        if (nranks < 1 || rank < 0 || rank >= nranks) cfg_err("comm_init: bad nranks / rank");
+        const NcclApi& a = nccl_or_throw();
+        if (ctx->comm) { a.comm_destroy(ctx->comm); ctx->comm = nullptr; }
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof id);
+        CK(cudaStreamSynchronize(ctx->stream));
+        nccl_check(a.comm_init_rank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+        ctx->comm_ranks = nranks;
+        ctx->comm_rank = rank;
+    });
+}
+
+int gsrc_comm_allreduce_grads(gsrc_ctx* ctx) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (!ctx->comm) seq_err("comm_allreduce_grads: no communicator (gsrc_comm_init)");
+        ctx->enqueue_allreduce();
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsrc_comm_destroy(gsrc_ctx* ctx) {
+    return guarded(ctx, [&] {
+        if (ctx->comm) {
+            CK(cudaStreamSynchronize(ctx->stream));
+            nccl_api().comm_destroy(ctx->comm);
+            ctx->comm = nullptr;
+        }
+        ctx->comm_ranks = 1;
+        ctx->comm_rank = 0;
+    });
+}
+
+// ---- reconstruction diagnostics -------------------------------------------------
+int gsrc_diag_masks(gsrc_ctx* ctx, int enable, int row_stride) {
+    return guarded(ctx, [&] {
+        ctx->require_model();
+        if (enable && ctx->cfg.mode != GSRC_MODE_GSRC) cfg_err("diag_masks: GSRC mode only");
+        if (enable && row_stride < 1) cfg_err("diag_masks: row_stride < 1");
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->diag_store) { cudaFree(ctx->diag_store); ctx->diag_store = nullptr; }
+        if (ctx->diag_cnt) { cudaFree(ctx->diag_cnt); ctx->diag_cnt = nullptr; }
+        ctx->diag = false;
+        ctx->drop_graphs();
+        if (!enable) return;
+        ctx->diag_stride = row_stride;
+        ctx->diag_rows = (ctx->n + row_stride - 1) / row_stride;
+        const size_t slots = static_cast<size_t>(ctx->cfg.layers) * ctx->C;
+        ctx->diag_store = dmalloc<uint4>(slots * static_cast<size_t>(ctx->diag_rows));
+        ctx->diag_cnt = dmalloc<unsigned long long>(slots);
+        CK(cudaMemset(ctx->diag_cnt, 0, sizeof(unsigned long long) * slots));
+        ctx->diag = true;
+    });
+}
+
+int gsrc_diag_mask_flips(gsrc_ctx* ctx, int64_t* flips, int64_t* sampled_rows) {
+    return guarded(ctx, [&] {
+        if (!ctx->diag) seq_err("diag_mask_flips: diagnostics not enabled (gsrc_diag_masks)");
+        const size_t slots = static_cast<size_t>(ctx->cfg.layers) * ctx->C;
+        std::vector<unsigned long long> h(slots);
+        CK(cudaMemcpyAsync(h.data(), ctx->diag_cnt, sizeof(unsigned long long) * slots, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (size_t q = 0; q < slots; ++q) flips[q] = static_cast<int64_t>(h[q]);
+        if (sampled_rows) *sampled_rows = ctx->diag_rows;
     });
 }
 

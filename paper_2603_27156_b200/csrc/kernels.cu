@@ -272,6 +272,8 @@ __global__ void k_scale(float* __restrict__ p, long long n, float s) {
 int sm_count();
 
 template <int W, int TPR>
+
+
 cudaError_t launch_gs_t(const GsArgs& a, cudaStream_t s) {
     constexpr int ROWS = kThreads / TPR;
     const int grid = (a.n + ROWS - 1) / ROWS;
@@ -296,6 +298,28 @@ int sm_count() {
         if (sms <= 0) sms = 148;
     }
     return sms;
+}
+
+// Mask-flip diagnostic (gsrc_diag_masks): the index bytes of sampled rows'
+// GS records (rows r = j·stride). mode 0 stores them (forward); mode 1 counts
+// the sampled rows whose recomputed mask differs (backward reconstruction).
+__global__ void k_diag_masks(const uint8_t* __restrict__ rec, int n, int stride, int rb, uint4* __restrict__ store, int mode,
+                             unsigned long long* __restrict__ counter) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long r = j * stride;
+    int diff = 0;
+    if (r < n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(rec + r * rb);
+        if (mode == 0) store[j] = v;
+        else {
+            const uint4 o = store[j];
+            diff = (v.x != o.x) | (v.y != o.y) | (v.z != o.z) | (v.w != o.w);
+        }
+    }
+    if (mode == 1) {
+        const int c = __syncthreads_count(diff);
+        if (threadIdx.x == 0 && c) atomicAdd(counter, static_cast<unsigned long long>(c));
+    }
 }
 
 inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
@@ -431,6 +455,14 @@ cudaError_t launch_sgd(float* p, const float* g, float* mom, long long n, float 
 cudaError_t launch_scale(float* p, long long n, float sc, cudaStream_t s) {
     if (!n) return cudaSuccess;
     k_scale<<<blocks_for(n, 256), 256, 0, s>>>(p, n, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag_masks(const uint8_t* rec, int n, int stride, int rb, uint4* store, int mode, unsigned long long* counter,
+                              cudaStream_t s) {
+    const long long m = (static_cast<long long>(n) + stride - 1) / stride;
+    if (!m) return cudaSuccess;
+    k_diag_masks<<<blocks_for(m, 256), 256, 0, s>>>(rec, n, stride, rb, store, mode, counter);
     return cudaGetLastError();
 }
 

@@ -156,6 +156,11 @@ cudaError_t launch_sum_double(const double* in, int n, double scale, double* out
 cudaError_t launch_sum_planes(const GsArgs& a, float* out, cudaStream_t s);
 cudaError_t launch_adam_prep(long long* t, double b1, double b2, float* bc, cudaStream_t s);
 
+// mask-flip diagnostic: store (mode 0) or compare-and-count (mode 1) the index
+// bytes of the GS records of rows r = j·stride
+cudaError_t launch_diag_masks(const std::uint8_t* rec, int n, int stride, int rb, uint4* store, int mode, unsigned long long* counter,
+                              cudaStream_t s);
+
 // records <-> host-layout helpers (parity entry points)
 cudaError_t launch_rec_unpack(const std::uint8_t* rec, int n, int k, float* vals, int* idx, cudaStream_t s);
 cudaError_t launch_rec_pack(const float* vals, const int* idx, int n, int k, std::uint8_t* rec, cudaStream_t s);

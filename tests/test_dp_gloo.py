@@ -135,3 +135,38 @@ def test_average_gradients_sum_then_exact_scale():
     x = torch.ones(4)
     with pytest.raises(Exception):
         dp.average_gradients(x)  # no process group: refuses instead of silently skipping
+
+
+class _FakeCommCtx:
+    """Records what init_native_comm hands the C-ABI (gsrc_comm_unique_id / gsrc_comm_init)."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+
+    def comm_unique_id(self):
+        return bytes([7] * 128)
+
+    def comm_init(self, uid, nranks, rank):
+        self.calls.append((uid, nranks, rank))
+
+
+def _comm_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_27156_b200.dp import DataParallelStep, init_native_comm
+    c = _FakeCommCtx(rank)
+    init_native_comm(c)
+    assert c.calls == [(bytes([7] * 128), world, rank)]
+    # gloo never takes the native path (it needs NCCL): the split path with a CPU gradient view
+    be = OracleBackend(rank)
+    step = DataParallelStep(be, lr=LR)
+    assert step.split and not step.native
+    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([1]))
+    dist.destroy_process_group()
+
+
+def test_native_comm_id_broadcast_world2(tmp_path):
+    world = 2
+    mp.spawn(_comm_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"ok{r}.npy").exists() for r in range(world))

@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 TF32_ROW_RTOL = 1e-4
 TF32_GRAD_RTOL = 1e-3   # one layer
 TF32_STEP_RTOL = 5e-3   # a multi-layer step: flipped near-tie masks compound across layers
+TF32_MAX_RTOL = 5e-2    # every row: one flipped near-tie column shifts a row by a fraction of one value's share
 
 
 @pytest.fixture(scope="module")
@@ -59,6 +60,7 @@ def _net(ctx, oracle, n, L, D, C, k, norm=1, hubs=(10, 60), hub_fraction=0.01, s
 
 def _rows_close(a, b):
     err = np.abs(a - b).max(1) / max(np.abs(b).max(), 1e-30)
+    assert err.max() <= TF32_MAX_RTOL, np.sort(err)[-10:]
     return (err <= TF32_ROW_RTOL).mean(), err
 
 
@@ -108,6 +110,7 @@ def test_fast_train_step(ctx, oracle_tf32, C, D, k, hubs, iso):
     # handful of predictions: bound the bulk, not the max
     close = np.abs(yhat - ryhat) <= TF32_ROW_RTOL * np.abs(ryhat).max()
     assert close.mean() >= 0.995, np.sort(np.abs(yhat - ryhat))[-10:]
+    assert np.abs(yhat - ryhat).max() <= TF32_MAX_RTOL * np.abs(ryhat).max()
     loss = ctx.forward_backward()
     rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
     assert abs(loss - rloss) <= TF32_STEP_RTOL * abs(rloss)
@@ -138,6 +141,7 @@ def test_fast_reversibility_roundtrip(ctx, oracle):
         ctx.layer_inverse(l)
     err = np.abs(ctx.activation() - x).max(1) / np.abs(y).max()
     assert (err <= 1e-4).mean() >= 0.999, np.sort(err)[-10:]
+    assert err.max() <= TF32_MAX_RTOL, np.sort(err)[-10:]
 
 
 def _det_setup(ctx, g, nd, p, graph):

@@ -264,6 +264,7 @@ def test_mem_peak_independent_of_depth(ctx, oracle):
 # layer; 1e-3 on losses / parameter gradients of a short network.
 TF32_ROW_RTOL = 1e-4
 TF32_GRAD_RTOL = 1e-3
+TF32_MAX_RTOL = 5e-2    # every row (a flipped near-tie column moves a row by a fraction of one value's share)
 
 
 @pytest.fixture
@@ -290,6 +291,7 @@ def test_tf32_layer_forward_inverse(ctx, oracle_tf32, C, D, k):
     row_err = np.abs(y - ry).max(1) / np.abs(ry).max()
     print("tf32 layer row err: median", np.median(row_err), "p99.5", np.quantile(row_err, 0.995), "max", row_err.max())
     assert (row_err <= TF32_ROW_RTOL).mean() >= 0.995, np.sort(row_err)[-20:]
+    assert row_err.max() <= TF32_MAX_RTOL
     w = D // C
     _, gi = oracle.gs_topk(y[:, :w], k)
     _, ri = oracle.gs_topk(ry[:, :w], k)
@@ -299,6 +301,7 @@ def test_tf32_layer_forward_inverse(ctx, oracle_tf32, C, D, k):
     # mask of the Eq. 6 group sum: bound the rows, not the max
     err = np.abs(ctx.activation() - x).max(1) / np.abs(y).max()
     assert (err <= TF32_ROW_RTOL).mean() >= 0.999, np.sort(err)[-10:]
+    assert err.max() <= TF32_MAX_RTOL
 
 
 def test_tf32_train_step(ctx, oracle_tf32):
