@@ -121,6 +121,16 @@ int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out);                    /* ker
    The activation arena is snapshotted and restored: no device state changes. */
 int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out);
 
+/* Exactly invertible residual stream (GSRC / REV modes; default shift 20). Each
+   block output h is rounded to the grid 2^-shift before the Eq. 6 add
+   (y = x + q(h)) and the Eq. 7 subtract, and the encoder output is put on the
+   same grid, so every residual add is exact for |x| < 2^(24-shift) and the
+   backward's inverse recompute reproduces each layer input
+   bit for bit at any depth: no reconstruction drift, no GS-mask flips. The
+   gradient treats q as the identity. shift 0 = plain fp32 adds (drifting). */
+int gsrc_set_residual_quant(gsrc_ctx* ctx, int shift);
+int gsrc_get_residual_quant(gsrc_ctx* ctx, int* shift);
+
 /* Optimizer state for exact resume (the GSRP checkpoint holds parameters
    only): Adam first/second moments and the step count. */
 int gsrc_optim_state_get(gsrc_ctx* ctx, float* m, float* v, int64_t* step, int64_t n);

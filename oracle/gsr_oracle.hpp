@@ -318,6 +318,19 @@ inline float tf32_op(float x) {
 }
 inline double tf32_op(double x) { return static_cast<double>(tf32_op(static_cast<float>(x))); }
 
+// Exactly invertible residual stream (the device's gsrc_set_residual_quant;
+// a B200-build extension): a block output h is rounded to
+// the grid 2^-s, half to even, before the Eq. 6 add / Eq. 7 subtract, and the
+// encoder output is put on the same grid. x + q(h) is then exact for
+// |x| < 2^(24-s) (f32), so rev_inverse_layer reproduces the forward input bit
+// for bit at any depth (SPEC.md:332-333,353 reversibility). s = 0: off.
+template <typename T>
+inline T quant(T h, int s) {
+    if (s <= 0) return h;
+    const T qs = std::ldexp(T(1), s), qi = std::ldexp(T(1), -s);
+    return std::nearbyint(h * qs) * qi;
+}
+
 // One row of a dense transform: out[j] = fma-chain_m a[m]*B(m,j) (+0 start).
 // B(m,j) = b[m*ldb + j] (plain) or b[j*ldb + m] (transposed operand).
 // rnd: TF32 operand rounding (see tf32_transform).
@@ -382,11 +395,11 @@ inline void transform_row(const T* z, int w, const T* W, const T* bias, BlockFla
 }
 
 template <typename T>
-inline void epilogue_row(int epi, const T* h, const T* R, const T* svals, const std::int32_t* sidx, int w, int k, T* out) {
+inline void epilogue_row(int epi, const T* h, const T* R, const T* svals, const std::int32_t* sidx, int w, int k, T* out, int qshift = 0) {
     switch (epi) {
         case EPI_NONE: for (int j = 0; j < w; ++j) out[j] = h[j]; break;
-        case EPI_ADD: for (int j = 0; j < w; ++j) out[j] = R[j] + h[j]; break;
-        case EPI_SUB: for (int j = 0; j < w; ++j) out[j] = R[j] - h[j]; break;
+        case EPI_ADD: for (int j = 0; j < w; ++j) out[j] = R[j] + quant(h[j], qshift); break;
+        case EPI_SUB: for (int j = 0; j < w; ++j) out[j] = R[j] - quant(h[j], qshift); break;
         case EPI_SCATTER_ADD:
         case EPI_SCATTER_SUB: {
             T sc[1024];
@@ -403,7 +416,7 @@ inline void epilogue_row(int epi, const T* h, const T* R, const T* svals, const 
 // out may alias R (in-place residual update is row-local).
 template <typename T>
 void gsr_block_apply(const Graph& g, int w, int k, const T* vals, const std::int32_t* idx, const T* W, const T* bias, BlockFlags f,
-                     int epi, const T* R, index_t ldr, const T* rvals, const std::int32_t* ridx, T* out, index_t ldo) {
+                     int epi, const T* R, index_t ldr, const T* rvals, const std::int32_t* ridx, T* out, index_t ldo, int qshift = 0) {
     Scales<T> s(g);
     auto d = direction(g, s, false);
     pfor(g.n, [&](index_t b, index_t e) {
@@ -411,7 +424,8 @@ void gsr_block_apply(const Graph& g, int w, int k, const T* vals, const std::int
         for (index_t r = b; r < e; ++r) {
             spmm_sparse_row(d, r, w, k, vals, idx, z);
             transform_row(z, w, W, bias, f, h);
-            epilogue_row(epi, h, R ? R + r * ldr : nullptr, rvals ? rvals + r * k : nullptr, ridx ? ridx + r * k : nullptr, w, k, out + r * ldo);
+            epilogue_row(epi, h, R ? R + r * ldr : nullptr, rvals ? rvals + r * k : nullptr, ridx ? ridx + r * k : nullptr, w, k, out + r * ldo,
+                         qshift);
         }
     });
     work().scalar_mul_adds += static_cast<std::uint64_t>(g.e) * k + (f.use_weight ? static_cast<std::uint64_t>(g.n) * w * w : 0);
@@ -420,7 +434,7 @@ void gsr_block_apply(const Graph& g, int w, int k, const T* vals, const std::int
 // dense_block: f(x) = spmm(g, relu(x))·W + b (ReLU input-side).
 template <typename T>
 void dense_block_apply(const Graph& g, int w, const T* x, index_t ldx, const T* W, const T* bias, BlockFlags f,
-                       int epi, const T* R, index_t ldr, T* out, index_t ldo) {
+                       int epi, const T* R, index_t ldr, T* out, index_t ldo, int qshift = 0) {
     Scales<T> s(g);
     auto d = direction(g, s, false);
     std::vector<T> rx(static_cast<size_t>(g.n) * w);
@@ -433,7 +447,7 @@ void dense_block_apply(const Graph& g, int w, const T* x, index_t ldx, const T* 
         for (index_t r = b; r < e; ++r) {
             spmm_row(d, r, w, rx.data(), w, z);
             transform_row(z, w, W, bias, f, h);
-            epilogue_row<T>(epi, h, R ? R + r * ldr : nullptr, nullptr, nullptr, w, 0, out + r * ldo);
+            epilogue_row<T>(epi, h, R ? R + r * ldr : nullptr, nullptr, nullptr, w, 0, out + r * ldo, qshift);
         }
     });
 }
@@ -511,6 +525,7 @@ struct NetCfg {
     int L = 0, D = 0, C = 2, k = 1, d_in = 1;
     BlockFlags flags{};
     int index_source = IDX_ALG2_LOCAL;
+    int qshift = 0;  // residual-stream grid 2^-qshift in the grouped-reversible modes (quant), 0 = off
 
     int groups() const { return mode == MODE_ALG12 ? 2 : C; }
     int width() const { return D / groups(); }
@@ -599,9 +614,10 @@ template <typename T>
 void apply_block(const Net<T>& net, int l, int i, const Act<T>& a, int epi, const T* R, index_t ldr, T* out, index_t ldo) {
     const int w = net.cfg.width();
     if (net.cfg.mode == MODE_REV)
-        dense_block_apply<T>(*net.g, w, a.dense.data(), w, net.W(l, i), net.B(l, i), net.cfg.flags, epi, R, ldr, out, ldo);
+        dense_block_apply<T>(*net.g, w, a.dense.data(), w, net.W(l, i), net.B(l, i), net.cfg.flags, epi, R, ldr, out, ldo, net.cfg.qshift);
     else
-        gsr_block_apply<T>(*net.g, w, net.cfg.k, a.vals.data(), a.idx.data(), net.W(l, i), net.B(l, i), net.cfg.flags, epi, R, ldr, nullptr, nullptr, out, ldo);
+        gsr_block_apply<T>(*net.g, w, net.cfg.k, a.vals.data(), a.idx.data(), net.W(l, i), net.B(l, i), net.cfg.flags, epi, R, ldr, nullptr, nullptr, out,
+                           ldo, net.cfg.qshift);
 }
 
 // Grouped reversible forward (Eq. 6; SPEC rev_forward_layer :316-324), in place.
@@ -671,7 +687,7 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
                 else spmm_sparse_row(fwd, r, w, k, a.vals.data(), a.idx.data(), z);
                 transform_row(z, w, net.W(l, i), net.B(l, i), f, h);
                 T* yr = Y + r * D + i * w;
-                for (int j = 0; j < w; ++j) yr[j] = yr[j] - h[j];
+                for (int j = 0; j < w; ++j) yr[j] = yr[j] - quant(h[j], net.cfg.qshift);
             }
         });
         T* Gi = G + i * w;
@@ -787,7 +803,8 @@ void encoder_forward(const Net<T>& net, const T* X0, T* X) {
     pfor(net.g->n, [&](index_t b, index_t e) {
         for (index_t r = b; r < e; ++r) {
             gemm_row(X0 + r * din, din, D, We, D, false, X + r * D);
-            for (int j = 0; j < D; ++j) X[r * D + j] = X[r * D + j] + be[j];
+            const int qs = net.cfg.mode == MODE_ALG12 ? 0 : net.cfg.qshift;  // grouped-reversible modes: on the residual grid
+            for (int j = 0; j < D; ++j) X[r * D + j] = quant(X[r * D + j] + be[j], qs);
         }
     });
 }

@@ -382,6 +382,14 @@ long long gsro_net_num_params(void* h) {
     return static_cast<Net<float>*>(box->net)->cfg.num_params();
 }
 
+int gsro_net_set_quant(void* h, int shift) {
+    auto* box = static_cast<NetBox*>(h);
+    if (shift < 0 || shift > 60) return 1;
+    if (box->is64) static_cast<Net<double>*>(box->net)->cfg.qshift = shift;
+    else static_cast<Net<float>*>(box->net)->cfg.qshift = shift;
+    return 0;
+}
+
 void gsro_net_destroy(void* h) {
     auto* box = static_cast<NetBox*>(h);
     if (!box) return;

@@ -254,7 +254,12 @@ def adam(p, g, m, v, t, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.0):
 class Net:
     """GSR / GSR-C / rev-baseline network."""
 
-    def __init__(self, g, mode, L, D, C_groups, k, d_in, use_weight=True, use_bias=False, index_source=0, dtype=np.float32):
+    # the device's default residual-stream grid (gsrc_set_residual_quant): f32
+    # nets in the grouped-reversible modes match it unless told otherwise; f64
+    # verification nets (finite differences, SPEC.md:658) keep plain adds
+    DEVICE_QSHIFT = 20
+
+    def __init__(self, g, mode, L, D, C_groups, k, d_in, use_weight=True, use_bias=False, index_source=0, dtype=np.float32, qshift=None):
         self.g = g
         self.dtype = np.dtype(dtype)
         self.sfx = _sfx(dtype)
@@ -265,6 +270,14 @@ class Net:
         self.mode, self.L, self.D, self.C, self.k, self.d_in = mode, L, D, C_groups, k, d_in
         self.n = g.n
         self.P = int(lib().gsro_net_num_params(self.h))
+        if qshift is None:
+            qshift = self.DEVICE_QSHIFT if (self.dtype == np.float32 and mode != MODE_ALG12) else 0
+        self.set_quant(qshift)
+
+    def set_quant(self, shift):
+        """Residual-stream grid 2^-shift (exactly invertible layers); 0 = plain adds."""
+        _chk(lib().gsro_net_set_quant(self.h, int(shift)))
+        self.qshift = int(shift)
 
     def _f(self, name):
         return getattr(lib(), f"gsro_net_{name}_{self.sfx}")

@@ -71,7 +71,8 @@ EXPORTS = [
     "gsrc_kernel_launches", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
     "gsrc_set_op_precision", "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
     "gsrc_get_stream", "gsrc_optim_state_get", "gsrc_optim_state_set", "gsrc_comm_unique_id", "gsrc_comm_init",
-    "gsrc_comm_allreduce_grads", "gsrc_comm_destroy", "gsrc_diag_masks", "gsrc_diag_mask_flips",
+    "gsrc_comm_allreduce_grads", "gsrc_comm_destroy", "gsrc_diag_masks", "gsrc_diag_mask_flips", "gsrc_set_residual_quant",
+    "gsrc_get_residual_quant",
 ]
 
 _lib = None
@@ -129,6 +130,8 @@ def lib():
         L.gsrc_comm_destroy.argtypes = [vp]
         L.gsrc_diag_masks.argtypes = [vp, i32, i32]
         L.gsrc_diag_mask_flips.argtypes = [vp, vp, C.POINTER(i64)]
+        L.gsrc_set_residual_quant.argtypes = [vp, i32]
+        L.gsrc_get_residual_quant.argtypes = [vp, C.POINTER(i32)]
         _lib = L
     return _lib
 
@@ -364,6 +367,15 @@ class Context:
 
     def comm_destroy(self):
         self._chk(lib().gsrc_comm_destroy(self.h))
+
+    def set_residual_quant(self, shift: int):
+        """Residual-stream grid 2^-shift (exactly invertible layers; 0 = plain fp32 adds)."""
+        self._chk(lib().gsrc_set_residual_quant(self.h, int(shift)))
+
+    def residual_quant(self) -> int:
+        s = C.c_int()
+        self._chk(lib().gsrc_get_residual_quant(self.h, C.byref(s)))
+        return s.value
 
     def diag_masks(self, enable=True, row_stride=1):
         self._chk(lib().gsrc_diag_masks(self.h, int(enable), int(row_stride)))

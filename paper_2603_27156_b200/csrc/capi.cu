@@ -166,6 +166,7 @@ struct gsrc_ctx {
     // their kSeg-edge segments (edge ranges) and each hub row's segment range
     int4* item_f = nullptr;  // sparse hub work items (launch_hub_rows)
     int* hcnt_f = nullptr;   // per hub: chunks finished (self-resetting)
+    int* hflag_f = nullptr;  // per hub: its Zh row is final (set by k_fast's hub phase, reset by the consuming tile)
     int2* seg_b = nullptr;   // dense hub segments {lo, hi} (launch_hub_dense)
     int *hub_b = nullptr, *segoff_b = nullptr;
     int nseg_f = 0, nseg_b = 0, nitem_f = 0;
@@ -235,7 +236,7 @@ struct gsrc_ctx {
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
         for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)ell_f, (void*)ell_b, (void*)item_f, (void*)seg_b, (void*)hub_b, (void*)segoff_b,
-                        (void*)hcnt_f, (void*)params, (void*)grads,
+                        (void*)hcnt_f, (void*)hflag_f, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
@@ -260,12 +261,18 @@ struct gsrc_ctx {
     Dir fwd() const { return Dir{rp, ci, row_f, col_f, norm != GSRC_NORM_SYM_DEGREE, ell_f}; }
     Dir bwd() const { return Dir{trp, tci, col_f, row_f, norm == GSRC_NORM_NONE, ell_b}; }
 
+    // exactly invertible residual stream (GSRC / REV): grid 2^-qshift, 0 = off
+    int qshift = 20;
+    float q_scale() const { return cfg.mode != GSRC_MODE_ALG12 && qshift > 0 ? std::ldexp(1.f, qshift) : 0.f; }
+    float q_inv() const { return cfg.mode != GSRC_MODE_ALG12 && qshift > 0 ? std::ldexp(1.f, -qshift) : 0.f; }
     TileArgs tile_base() const {
         TileArgs a;
         a.n = static_cast<int>(n);
         a.w = w;
         a.ld = ld;
         a.tc = cfg.gemm == GSRC_GEMM_TF32;
+        a.qs = q_scale();
+        a.qi = q_inv();
         return a;
     }
     int last_grid = 0;
@@ -353,6 +360,8 @@ struct gsrc_ctx {
         f.k = k;
         f.dir = transpose ? bwd() : fwd();
         f.Zh = Zh;
+        f.qs = q_scale();
+        f.qi = q_inv();
         return f;
     }
     float* Pseg = nullptr;  // hub segment partials (arena)
@@ -375,10 +384,18 @@ struct gsrc_ctx {
         ++launches;
     }
     // f_i with Eq. 6 add (+ GS of the output for the next block)
+    // sparse hub rows: computed by the FWD / INV kernel itself before its tiles
+    void with_sparse_hubs(FastArgs& f) const {
+        f.hub_items = item_f;
+        f.nhub_items = nitem_f;
+        f.hub_cnt = hcnt_f;
+        f.hub_flag = hflag_f;
+        f.Pseg = Pseg;
+    }
     void fast_block_forward(int l, int i, const uint8_t* rec, uint8_t* gs_out) {
         FastArgs f = fast_base(false);
         f.rec_in = rec;
-        run_hub(true, f, false);
+        with_sparse_hubs(f);
         f.Wm = Wb(l, i);
         f.bias = Bb(l, i);
         f.R = plane(X, i);
@@ -404,7 +421,7 @@ struct gsrc_ctx {
     void fast_inverse(int l, int i, const uint8_t* rec, uint8_t* gs_out = nullptr) {
         FastArgs f = fast_base(false);
         f.rec_in = rec;
-        run_hub(true, f, false);
+        with_sparse_hubs(f);
         f.Wm = Wb(l, i);
         f.bias = Bb(l, i);
         f.R = plane(X, i);
@@ -524,8 +541,9 @@ struct gsrc_ctx {
             if (i > 0) u = plane(X, i - 1);
             else { run_sum_planes(X, U); u = U; }
         }
-        if (fast() && cfg.use_weight && with_grads) {
-            fast_block_backward(l, i, recA);
+        if (fast() && cfg.use_weight) {  // the same tensor-core kernels as the forward: an exact inverse on the residual grid
+            if (with_grads) fast_block_backward(l, i, recA);
+            else fast_inverse(l, i, recA);
             return;
         }
         TileArgs a = tile_base();
@@ -629,7 +647,7 @@ struct gsrc_ctx {
     void enqueue_forward() {
         if (diag) CK(cudaMemsetAsync(diag_cnt, 0, sizeof(unsigned long long) * static_cast<size_t>(cfg.layers) * C, stream));
         CK(launch_encoder(X0, static_cast<int>(n), cfg.d_in, params, params + static_cast<size_t>(cfg.d_in) * cfg.hidden, cfg.hidden,
-                          C, w, ld, X, stream));
+                          C, w, ld, X, q_scale(), q_inv(), stream));
         ++launches;
         if (cfg.mode == GSRC_MODE_ALG12) std::fill(filled.begin(), filled.end(), 0);
         for (int l = 0; l < cfg.layers; ++l) layer_forward(l);
@@ -928,16 +946,18 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
-        for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
+        for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->hflag_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
                         (void*)ctx->ell_f, (void*)ctx->ell_b})
             if (p) cudaFree(p);
         // per-row neighbour slots (Dir::ell): edge scale = the direction's edge_f of the neighbour
+        // hub rows: {-2, hub index} in slot 0 (the index into that direction's hub list)
         auto ell_table = [&](const std::vector<int>& ptr, const int* idx, const std::vector<float>& ef) {
             std::vector<int2> t(static_cast<size_t>(n) * kAggSeg, make_int2(-1, 0));
+            int nh = 0;
             for (int64_t r = 0; r < n; ++r) {
                 int2* s = t.data() + static_cast<size_t>(r) * kAggSeg;
                 const int e0 = ptr[static_cast<size_t>(r)], e1 = ptr[static_cast<size_t>(r) + 1];
-                if (e1 - e0 > kAggSeg) { s[0].x = -2; continue; }
+                if (e1 - e0 > kAggSeg) { s[0] = make_int2(-2, nh++); continue; }
                 for (int q = e0; q < e1; ++q) {
                     float f = ef[static_cast<size_t>(idx[q])];
                     int bits;
@@ -973,6 +993,8 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (!hubs.empty()) CK(cudaMemset(cnt, 0, sizeof(int) * hubs.size()));
         };
         hub_table(hf, rp, kHubChunk, ctx->item_f, ctx->nitem_f, ctx->hcnt_f, ctx->nseg_f);
+        ctx->hflag_f = dmalloc<int>(std::max<size_t>(hf.size(), 1), &ctx->graph_bytes);
+        CK(cudaMemset(ctx->hflag_f, 0, sizeof(int) * std::max<size_t>(hf.size(), 1)));
         {  // dense: flattened segments, per-hub first segment
             std::vector<int2> sv;
             std::vector<int> ov(hb.size() + 1, 0);
@@ -1592,6 +1614,17 @@ int gsrc_profile_kernels(gsrc_ctx* ctx, int reps, double* out) {
         out[15] = 0;
     });
 }
+
+int gsrc_set_residual_quant(gsrc_ctx* ctx, int shift) {
+    return guarded(ctx, [&] {
+        if (shift < 0 || shift > 30) cfg_err("residual quant: shift must be in [0, 30] (0 = off)");
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->qshift = shift;
+        ctx->drop_graphs();
+    });
+}
+
+int gsrc_get_residual_quant(gsrc_ctx* ctx, int* shift) { return guarded(ctx, [&] { *shift = ctx->qshift; }); }
 
 int gsrc_get_stream(gsrc_ctx* ctx, void** out) {
     return guarded(ctx, [&] {

@@ -13,6 +13,13 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// Exactly invertible residual stream (gsrc_set_residual_quant): the block
+// output h is rounded to the grid 2^-s (round half to even) before the Eq. 6
+// add / Eq. 7 subtract, so x + q(h) and (x + q(h)) − q(h) are exact for |x| <
+// 2^(24-s) and the inverse recompute reproduces the forward bit for bit.
+// qs = 2^s, qi = 2^-s; qs == 0 disables it. Both multiplies are exact.
+__device__ __forceinline__ float quant(float h, float qs, float qi) { return qs != 0.f ? __fmul_rn(rintf(__fmul_rn(h, qs)), qi) : h; }
+
 // Programmatic dependent launch (launch_pdl): a kernel launched with it may
 // start while its stream predecessor finishes. pdl_wait() blocks until the
 // predecessor has completed and its memory is visible — every PDL kernel calls

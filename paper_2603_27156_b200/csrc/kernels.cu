@@ -146,14 +146,14 @@ __global__ void k_rec_pack(const float* __restrict__ vals, const int* __restrict
 // ---------------------------------------------------------------------------
 // X[p][r][m] = fma-chain_a X0[r][a]·We[a][p·w+m] + be[p·w+m]
 __global__ void k_encoder(const float* __restrict__ X0, int n, int d_in, const float* __restrict__ We, const float* __restrict__ be,
-                          int D, int w, int ld, float* __restrict__ X) {
+                          int D, int w, int ld, float* __restrict__ X, float qs, float qi) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<long long>(n) * D) return;
     const int r = static_cast<int>(i / D), col = static_cast<int>(i % D);
     const int p = col / w, m = col % w;
     float acc = 0.f;
     for (int t = 0; t < d_in; ++t) acc = fmaf(__ldg(X0 + static_cast<size_t>(r) * d_in + t), __ldg(We + static_cast<size_t>(t) * D + col), acc);
-    X[(static_cast<size_t>(p) * n + r) * ld + m] = __fadd_rn(acc, __ldg(be + col));
+    X[(static_cast<size_t>(p) * n + r) * ld + m] = dev::quant(__fadd_rn(acc, __ldg(be + col)), qs, qi);  // on the residual grid
 }
 
 // ŷ[r] = fma-chain_n X[r][n]·wh[n] + bh; masked MSE gradient and loss partials.
@@ -406,11 +406,11 @@ cudaError_t launch_rec_pack(const float* vals, const int* idx, int n, int k, uin
 }
 
 cudaError_t launch_encoder(const float* X0, int n, int d_in, const float* We, const float* be, int D, int C, int w, int ld, float* X,
-                           cudaStream_t s) {
+                           float qs, float qi, cudaStream_t s) {
     (void)C;
     const long long tot = static_cast<long long>(n) * D;
     if (!tot) return cudaSuccess;
-    k_encoder<<<blocks_for(tot, 256), 256, 0, s>>>(X0, n, d_in, We, be, D, w, ld, X);
+    k_encoder<<<blocks_for(tot, 256), 256, 0, s>>>(X0, n, d_in, We, be, D, w, ld, X, qs, qi);
     return cudaGetLastError();
 }
 

@@ -87,6 +87,7 @@ struct TileArgs {
     int want_db = 0;
     double* part = nullptr;                // [gridDim.x][w*w + w]
     int tc = 0;                            // 1: transform on tcgen05 (TF32), 0: FP32-strict FFMA
+    float qs = 0.f, qi = 0.f;              // EPI_ADD / EPI_SUB: residual-stream grid 2^-s (dev::quant); 0 = off
 };
 
 // Thread-per-row tcgen05 fast path (fast.cu) for the GSR-C step in TF32 mode.
@@ -111,8 +112,19 @@ struct FastArgs {
     int k_m = 0;
     float* dst[kMaxDst] = {};
     int ndst = 0;
+    // FWD / INV sparse hub rows (deg > kAggSeg), computed inside k_fast before
+    // its tiles: work items {row, first edge, end edge, first segment}, {hub,
+    // the row's first partial in Pseg}; hub_cnt[hub] = chunks finished (reset by
+    // the folding chunk); hub_flag[hub] = 1 once Zh[row] is final (reset by the
+    // tile that consumes it). The hub index of a row is in its ELL slot 0 (.y).
+    const int4* hub_items = nullptr;
+    int nhub_items = 0;
+    int* hub_cnt = nullptr;
+    int* hub_flag = nullptr;
+    float* Pseg = nullptr;
     CUtensorMap tm_x;                      // FWD / INV: 2-D tiled map of the R/out plane (128 rows × 32 cols, SWIZZLE_128B)
     CUtensorMap tm_dst[kMaxDst];           // BIN: maps of the dst planes (TMA reduce-add of the masked gradient tile)
+    float qs = 0.f, qi = 0.f;              // FWD / INV: residual-stream grid 2^-s (dev::quant); 0 = off
 };
 
 bool fast_supported(int w, int k);
@@ -167,7 +179,7 @@ cudaError_t launch_rec_pack(const float* vals, const int* idx, int n, int k, std
 
 // encoder / head / loss / optimizer
 cudaError_t launch_encoder(const float* X0, int n, int d_in, const float* We, const float* be, int D, int C, int w, int ld,
-                           float* X, cudaStream_t s);
+                           float* X, float qs, float qi, cudaStream_t s);
 cudaError_t launch_head_loss(const float* X, int n, int D, int C, int w, int ld, const float* wh, const float* bh,
                              const float* y, const std::uint8_t* mask, float inv_cnt_unused, float cnt, float* yhat, float* gy,
                              double* loss_part, int nparts, cudaStream_t s);

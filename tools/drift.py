@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--stride", type=int, default=1)
     ap.add_argument("--lr-sweep", default="")
     ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--qshift", type=int, default=20, help="residual-stream grid 2^-qshift (0 = plain fp32 adds)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     from paper_2603_27156_b200 import GEMM_FP32, GEMM_TF32, MODE_GSRC, Context, model, synth
@@ -47,20 +48,31 @@ def main():
     p = model.init_params(MODE_GSRC, L, D, C, d_in, seed=1)
     ctx.set_params(p)
     ctx.data_upload(nd.features, nd.labels, nd.train_mask)
+    ctx.set_residual_quant(a.qshift)
     ctx.diag_masks(True, a.stride)
     loss = ctx.forward_backward()
     flips, rows = ctx.mask_flips()
     xr = ctx.activation()  # the backward sweep leaves the reconstructed encoder output
-    xenc = nd.features.astype(np.float64) @ p[:d_in * D].reshape(d_in, D).astype(np.float64) + p[d_in * D:d_in * D + D]
+    # the encoder output itself: a 0-layer model with the same encoder / head on the device
+    enc = Context(0)
+    enc.graph_upload(g.row_ptr, g.col_idx, norm=1)
+    enc.model_init(MODE_GSRC, 0, D, C, k, d_in, gemm=GEMM_TF32 if a.gemm == "tf32" else GEMM_FP32)
+    enc.set_residual_quant(a.qshift)
+    lay = model.param_layout(MODE_GSRC, L, D, C, d_in)
+    enc.set_params(np.concatenate([p[:d_in * D + D], p[lay["head_w"][0]:]]))
+    enc.data_upload(nd.features, nd.labels, nd.train_mask)
+    enc.forward()
+    xenc = enc.activation()
+    enc.close()
     err = np.abs(xr - xenc).max(1) / np.abs(xenc).max()
     rate = flips / rows
     res = {
-        "config": a.config, "gemm": a.gemm, "n": g.n, "e": g.e, "layers": L, "groups": C, "k": k, "row_stride": a.stride,
+        "config": a.config, "gemm": a.gemm, "qshift": a.qshift, "max_abs_activation": float(np.abs(xr).max()), "n": g.n, "e": g.e, "layers": L, "groups": C, "k": k, "row_stride": a.stride,
         "sampled_rows_per_block": int(rows), "loss": loss,
         "mask_flip_rate": {"mean": float(rate.mean()), "max": float(rate.max()), "total_flipped_rows": int(flips.sum()),
                            "per_layer_mean": [float(x) for x in rate.mean(1)],
                            "block0_mean": float(rate[:, 0].mean()), "blocks_ge1_mean": float(rate[:, 1:].mean())},
-        "reconstruction": {"max_rel": float(err.max()), "rows_over_1e-4": float((err > 1e-4).mean()),
+        "reconstruction": {"bit_exact": bool(np.array_equal(xr, xenc)), "max_rel": float(err.max()), "rows_over_1e-4": float((err > 1e-4).mean()),
                            "rows_over_1e-6": float((err > 1e-6).mean()), "median_rel": float(np.median(err))},
     }
     ctx.diag_masks(False)
