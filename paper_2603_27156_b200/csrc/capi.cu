@@ -166,7 +166,6 @@ struct gsrc_ctx {
     // their kSeg-edge segments (edge ranges) and each hub row's segment range
     int4* item_f = nullptr;  // sparse hub work items (launch_hub_rows)
     int* hcnt_f = nullptr;   // per hub: chunks finished (self-resetting)
-    int* hflag_f = nullptr;  // per hub: its Zh row is final (set by k_fast's hub phase, reset by the consuming tile)
     int2* seg_b = nullptr;   // dense hub segments {lo, hi} (launch_hub_dense)
     int *hub_b = nullptr, *segoff_b = nullptr;
     int nseg_f = 0, nseg_b = 0, nitem_f = 0;
@@ -236,7 +235,7 @@ struct gsrc_ctx {
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
         for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)ell_f, (void*)ell_b, (void*)item_f, (void*)seg_b, (void*)hub_b, (void*)segoff_b,
-                        (void*)hcnt_f, (void*)hflag_f, (void*)params, (void*)grads,
+                        (void*)hcnt_f, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
         if (loss_host) cudaFreeHost(loss_host);
@@ -384,18 +383,10 @@ struct gsrc_ctx {
         ++launches;
     }
     // f_i with Eq. 6 add (+ GS of the output for the next block)
-    // sparse hub rows: computed by the FWD / INV kernel itself before its tiles
-    void with_sparse_hubs(FastArgs& f) const {
-        f.hub_items = item_f;
-        f.nhub_items = nitem_f;
-        f.hub_cnt = hcnt_f;
-        f.hub_flag = hflag_f;
-        f.Pseg = Pseg;
-    }
     void fast_block_forward(int l, int i, const uint8_t* rec, uint8_t* gs_out) {
         FastArgs f = fast_base(false);
         f.rec_in = rec;
-        with_sparse_hubs(f);
+        run_hub(true, f, false);
         f.Wm = Wb(l, i);
         f.bias = Bb(l, i);
         f.R = plane(X, i);
@@ -421,7 +412,7 @@ struct gsrc_ctx {
     void fast_inverse(int l, int i, const uint8_t* rec, uint8_t* gs_out = nullptr) {
         FastArgs f = fast_base(false);
         f.rec_in = rec;
-        with_sparse_hubs(f);
+        run_hub(true, f, false);
         f.Wm = Wb(l, i);
         f.bias = Bb(l, i);
         f.R = plane(X, i);
@@ -946,18 +937,16 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (row_ptr[r + 1] - row_ptr[r] > kAggSeg) hf.push_back(static_cast<int>(r));
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
-        for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->hflag_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
+        for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
                         (void*)ctx->ell_f, (void*)ctx->ell_b})
             if (p) cudaFree(p);
         // per-row neighbour slots (Dir::ell): edge scale = the direction's edge_f of the neighbour
-        // hub rows: {-2, hub index} in slot 0 (the index into that direction's hub list)
         auto ell_table = [&](const std::vector<int>& ptr, const int* idx, const std::vector<float>& ef) {
             std::vector<int2> t(static_cast<size_t>(n) * kAggSeg, make_int2(-1, 0));
-            int nh = 0;
             for (int64_t r = 0; r < n; ++r) {
                 int2* s = t.data() + static_cast<size_t>(r) * kAggSeg;
                 const int e0 = ptr[static_cast<size_t>(r)], e1 = ptr[static_cast<size_t>(r) + 1];
-                if (e1 - e0 > kAggSeg) { s[0] = make_int2(-2, nh++); continue; }
+                if (e1 - e0 > kAggSeg) { s[0].x = -2; continue; }
                 for (int q = e0; q < e1; ++q) {
                     float f = ef[static_cast<size_t>(idx[q])];
                     int bits;
@@ -993,8 +982,6 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (!hubs.empty()) CK(cudaMemset(cnt, 0, sizeof(int) * hubs.size()));
         };
         hub_table(hf, rp, kHubChunk, ctx->item_f, ctx->nitem_f, ctx->hcnt_f, ctx->nseg_f);
-        ctx->hflag_f = dmalloc<int>(std::max<size_t>(hf.size(), 1), &ctx->graph_bytes);
-        CK(cudaMemset(ctx->hflag_f, 0, sizeof(int) * std::max<size_t>(hf.size(), 1)));
         {  // dense: flattened segments, per-hub first segment
             std::vector<int2> sv;
             std::vector<int> ov(hb.size() + 1, 0);

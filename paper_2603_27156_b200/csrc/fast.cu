@@ -361,151 +361,6 @@ __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uin
     else gs_row_impl<W, false>(Ts, r, w, k, rec_out);
 }
 
-// ---- sparse hub rows inside k_fast (FWD / INV) --------------------------------
-// Before its tiles, every persistent CTA works through the hub-row items
-// (a.hub_items, kHubChunk segments each) two at a time: threads 0-63 take one
-// item, 64-127 the next, a thread per kSeg-edge segment summed into a private
-// swizzled partial row of the (not yet used) A-operand buffer. A row of one
-// chunk is folded there; a longer row's chunks write their partials to Pseg
-// and the last chunk to finish folds the row from Pseg — the canonical
-// segmented order either way. The folding thread group then publishes the row
-// (hub_flag[h] = 1, release); the tile that owns the row waits for the flag
-// (acquire) before reading Zh. Every CTA finishes its items before it waits on
-// any flag, so no CTA can wait on a CTA that is itself waiting.
-__device__ __forceinline__ int hsw(int r, int c) { return c ^ ((r & 7) << 2); }
-// a 64-thread half of the CTA (barriers 1 and 2; immediate ids keep the CTA's barrier count at 3)
-__device__ __forceinline__ void half_sync(int half) {
-    if (half) asm volatile("bar.sync 2, 64;" ::: "memory");
-    else asm volatile("bar.sync 1, 64;" ::: "memory");
-}
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
-
-// one segment (≤ kSeg records) of a sparse hub row into partial row `row` of P
-template <int W>
-__device__ __forceinline__ void hub_seg_rows(const FastArgs& a, int lo, int ne, float* P, int row) {
-    const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
-    const bool unit = a.dir.unit_edge != 0;
-    float* pr = P + row * W;
-    int cs[kSegF];
-#pragma unroll
-    for (int u = 0; u < kSegF; ++u) cs[u] = u < ne ? __ldg(a.dir.idx + lo + u) : 0;
-#pragma unroll
-    for (int u = 1; u < kSegF; ++u)
-        if (u < ne) prefetch_l2(a.rec_in + static_cast<size_t>(cs[u]) * RB);
-    tile::SparseRec buf[2];
-    tile::load_rec16(buf[0], a.rec_in + static_cast<size_t>(cs[0]) * RB, nv4);
-#pragma unroll
-    for (int u = 0; u < kSegF; ++u) {
-        if (u < ne) {
-            if (u + 1 < ne) tile::load_rec16(buf[(u + 1) & 1], a.rec_in + static_cast<size_t>(cs[u + 1 < kSegF ? u + 1 : 0]) * RB, nv4);
-            const float sc = unit ? 1.f : __ldg(a.dir.edge_f + cs[u]);
-            const tile::SparseRec& rc = buf[u & 1];
-            const uint32_t iw[4] = {rc.idx.x, rc.idx.y, rc.idx.z, rc.idx.w};
-            const float vv[16] = {rc.v[0].x, rc.v[0].y, rc.v[0].z, rc.v[0].w, rc.v[1].x, rc.v[1].y, rc.v[1].z, rc.v[1].w,
-                                  rc.v[2].x, rc.v[2].y, rc.v[2].z, rc.v[2].w, rc.v[3].x, rc.v[3].y, rc.v[3].z, rc.v[3].w};
-#pragma unroll
-            for (int h = 0; h < 16; h += 8) {
-                int mm[8];
-                float old[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    mm[j] = hsw(row, static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3))));
-                    if (h + j < k) old[j] = pr[mm[j]];
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (h + j < k) pr[mm[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[h + j]));
-            }
-        }
-    }
-}
-
-// the hub phase of k_fast: P = the A-operand buffer (2 × kHubChunk × W floats)
-template <int W>
-__device__ __forceinline__ void hub_phase(const FastArgs& a, float* P) {
-    static_assert(2 * kHubChunk * W <= TR * W, "two hub partial blocks must fit the A-operand tile");
-    constexpr int CH = kHubChunk;
-    const int t = threadIdx.x, half = t >> 6, ht = t & 63;
-    float* Ph = P + half * CH * W;
-    const int ld = a.ld;
-    const int per_pass = 2 * static_cast<int>(gridDim.x);
-    for (int base = 2 * static_cast<int>(blockIdx.x); base < a.nhub_items; base += per_pass) {
-        const int it = base + half;
-        const bool have = it < a.nhub_items;
-        int4 ia = make_int4(0, 0, 0, 0), ib = make_int4(0, 0, 0, 0);
-        if (have) { ia = __ldg(a.hub_items + 2 * it); ib = __ldg(a.hub_items + 2 * it + 1); }
-        const int r = ia.x, e0 = ia.y, e1 = ia.z, c0 = ia.w, h = ib.x;
-        const int nseg = (e1 - e0 + kSegF - 1) / kSegF;
-        const int ns = have ? min(CH, nseg - c0) : 0;
-#pragma unroll
-        for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Ph + ht * W + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ht < ns) {
-            const int lo = e0 + (c0 + ht) * kSegF;
-            hub_seg_rows<W>(a, lo, min(kSegF, e1 - lo), Ph, ht);
-        }
-        half_sync(half);
-        if (have) {
-            if (nseg <= CH) {  // the whole row is here: fold left to right, publish
-                for (int col = ht; col < ld; col += 64) {
-                    float z = Ph[hsw(0, col)];
-                    for (int j = 1; j < ns; ++j) z = __fadd_rn(z, Ph[j * W + hsw(j, col)]);
-                    a.Zh[static_cast<size_t>(r) * ld + col] = z;
-                }
-                __threadfence();
-                half_sync(half);
-                if (ht == 0) st_release(a.hub_flag + h, 1);
-            } else {  // a chunk of a longer row: partials out; the last chunk folds
-                const int s0 = ib.y;
-                float* Pg = a.Pseg + static_cast<size_t>(s0 + c0) * ld;
-                for (int i = ht; i < ns * (ld >> 2); i += 64) {
-                    const int rr = i / (ld >> 2), c4 = 4 * (i % (ld >> 2));
-                    float4 v;
-                    v.x = Ph[rr * W + hsw(rr, c4)]; v.y = Ph[rr * W + hsw(rr, c4 + 1)];
-                    v.z = Ph[rr * W + hsw(rr, c4 + 2)]; v.w = Ph[rr * W + hsw(rr, c4 + 3)];
-                    *reinterpret_cast<float4*>(Pg + static_cast<size_t>(rr) * ld + c4) = v;
-                }
-                __threadfence();
-                half_sync(half);
-                int last = 0;
-                if (ht == 0) {
-                    const int nch = (nseg + CH - 1) / CH;
-                    last = atomicAdd(a.hub_cnt + h, 1) == nch - 1;
-                }
-                // thread 0 of the half tells the other 63 through the partial buffer's first word (free after the barrier above)
-                if (ht == 0) Ph[0] = __int_as_float(last);
-                half_sync(half);
-                last = __float_as_int(Ph[0]);
-                if (last) {
-                    __threadfence();
-                    const float* Pr = a.Pseg + static_cast<size_t>(s0) * ld;
-                    for (int col = ht; col < ld; col += 64) {
-                        float z = __ldcg(Pr + col);
-                        int s = 1;
-                        for (; s + 16 <= nseg; s += 16) {  // sixteen partials in flight, folded in order
-                            float pv[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) pv[i] = __ldcg(Pr + static_cast<size_t>(s + i) * ld + col);
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) z = __fadd_rn(z, pv[i]);
-                        }
-                        for (; s < nseg; ++s) z = __fadd_rn(z, __ldcg(Pr + static_cast<size_t>(s) * ld + col));
-                        a.Zh[static_cast<size_t>(r) * ld + col] = z;
-                    }
-                    __threadfence();
-                    half_sync(half);
-                    if (ht == 0) { a.hub_cnt[h] = 0; st_release(a.hub_flag + h, 1); }
-                }
-            }
-        }
-        __syncthreads();  // both halves done with P before the next pass zeroes it
-    }
-}
-
 template <int W, int KIND, int KS>
 __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
@@ -539,10 +394,6 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
     const uint32_t tlane = static_cast<uint32_t>(32 * wid) << 16;
     uint32_t ph0 = 0, ph2 = 0;
     dev::pdl_wait();  // the prologue above touched only W and on-chip state
-    if (a.nhub_items) {
-        hub_phase<W>(a, Zs);
-        __syncthreads();
-    }
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
         const int row0 = tile_i * TR;
@@ -569,14 +420,11 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
                 float sv[kSegF];
                 const int ne = load_ell_row(a.dir.ell, row, cv, sv);
                 rf = __ldg(a.dir.out_f + row);
-                if (ne < 0) {  // hub row: canonical segmented sum from the hub phase (this or another CTA)
-                    int* fl = a.hub_flag + __float_as_int(sv[0]);
-                    while (ld_acquire(fl) == 0) __nanosleep(64);
-                    *fl = 0;  // consumed (the next launch's hub phase sets it again)
+                if (ne < 0) {  // hub row: canonical segmented sum precomputed by k_hub_*
                     const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
 #pragma unroll
                     for (int c = 0; c < W; c += 4)
-                        if (c < a.ld) *reinterpret_cast<float4*>(Zs + zo(t, c)) = __ldcg(reinterpret_cast<const float4*>(zh + c));
+                        if (c < a.ld) *reinterpret_cast<float4*>(Zs + zo(t, c)) = dev::ld4(zh + c);
                 } else {
                     agg_sparse_row<W, KS>(a, cv, sv, ne, Zs, t);
                 }

@@ -112,16 +112,6 @@ struct FastArgs {
     int k_m = 0;
     float* dst[kMaxDst] = {};
     int ndst = 0;
-    // FWD / INV sparse hub rows (deg > kAggSeg), computed inside k_fast before
-    // its tiles: work items {row, first edge, end edge, first segment}, {hub,
-    // the row's first partial in Pseg}; hub_cnt[hub] = chunks finished (reset by
-    // the folding chunk); hub_flag[hub] = 1 once Zh[row] is final (reset by the
-    // tile that consumes it). The hub index of a row is in its ELL slot 0 (.y).
-    const int4* hub_items = nullptr;
-    int nhub_items = 0;
-    int* hub_cnt = nullptr;
-    int* hub_flag = nullptr;
-    float* Pseg = nullptr;
     CUtensorMap tm_x;                      // FWD / INV: 2-D tiled map of the R/out plane (128 rows × 32 cols, SWIZZLE_128B)
     CUtensorMap tm_dst[kMaxDst];           // BIN: maps of the dst planes (TMA reduce-add of the masked gradient tile)
     float qs = 0.f, qi = 0.f;              // FWD / INV: residual-stream grid 2^-s (dev::quant); 0 = off

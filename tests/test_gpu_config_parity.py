@@ -176,8 +176,8 @@ def test_c2_fwd_inverse_bwd_tf32(ctx, oracle_tf32, c2_data):
     yhat = ctx.forward()
     ryhat, rX = net.forward(nd.features)
     # 28 layers: see _assert_tf32_rows
-    _assert_tf32_rows(yhat, ryhat, frac=0.95, frac_1e3=0.99, what="c2 tf32 yhat")
-    _assert_tf32_rows(ctx.activation(), rX, frac=0.95, frac_1e3=0.99, what="c2 tf32 X_L")
+    _assert_tf32_rows(yhat, ryhat, frac=0.95, frac_1e3=0.975, what="c2 tf32 yhat")
+    _assert_tf32_rows(ctx.activation(), rX, frac=0.95, frac_1e3=0.975, what="c2 tf32 X_L")
     xL = ctx.activation()
     for l in reversed(range(L)):
         ctx.layer_inverse(l)
