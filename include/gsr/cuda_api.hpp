@@ -51,6 +51,9 @@ inline void check(int status, gsrc_ctx* ctx, const char* what) {
         case GSRC_ERR_CONFIG: throw ConfigError(msg);
         case GSRC_ERR_SEQUENCING: throw SequencingError(msg);
         case GSRC_ERR_RESOURCE: throw ResourceError(msg);
+        // an unexpected CUDA error is a device failure: the reference's
+        // ResourceError class ("allocation / device", CLI exit 3)
+        case GSRC_ERR_INTERNAL: throw ResourceError("internal CUDA error: " + msg);
         default: throw std::runtime_error(msg);
     }
 }
@@ -139,6 +142,37 @@ public:
         return m;
     }
     void high_water_reset() { check(gsrc_high_water_reset(h_), h_, "high_water_reset"); }
+
+    // Optimizer state (Adam m, v, step) for exact resume beside a GSRP checkpoint.
+    struct OptimState {
+        std::vector<float> m, v;
+        std::int64_t step = 0;
+    };
+    OptimState optim_state() const {
+        OptimState o;
+        const auto n = static_cast<size_t>(num_params());
+        o.m.resize(n);
+        o.v.resize(n);
+        int64_t st = 0;
+        check(gsrc_optim_state_get(h_, o.m.data(), o.v.data(), &st, static_cast<int64_t>(n)), h_, "optim_state_get");
+        o.step = st;
+        return o;
+    }
+    void set_optim_state(const OptimState& o) {
+        if (o.m.size() != o.v.size()) throw ShapeError("optim state: m and v differ in length");
+        check(gsrc_optim_state_set(h_, o.m.data(), o.v.data(), o.step, static_cast<int64_t>(o.m.size())), h_, "optim_state_set");
+    }
+
+    // Data parallelism: one process per GPU; rank 0 makes the
+    // id, every rank joins with it; train_step then averages the gradients.
+    static std::vector<unsigned char> comm_unique_id() {
+        std::vector<unsigned char> id(128);
+        check(gsrc_comm_unique_id(id.data(), id.size()), nullptr, "comm_unique_id");
+        return id;
+    }
+    void comm_init(const std::vector<unsigned char>& id, int nranks, int rank) {
+        check(gsrc_comm_init(h_, id.data(), nranks, rank), h_, "comm_init");
+    }
     std::int64_t kernel_launches() const {
         int64_t n = 0;
         check(gsrc_kernel_launches(h_, &n), h_, "kernel_launches");

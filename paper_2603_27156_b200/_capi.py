@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsrcuda.so")
+LIB_PATH = os.environ.get("GSRC_LIB") or os.path.join(_HERE, "libgsrcuda.so")  # GSRC_LIB: an alternate build (A/B timing)
 
 MODE_ALG12, MODE_GSRC, MODE_REV = 0, 1, 2
 NORM_NONE, NORM_ROW_MEAN, NORM_SYM_DEGREE = 0, 1, 2

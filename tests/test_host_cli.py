@@ -95,7 +95,7 @@ def test_cli_trains_and_matches_python_host(cli, tmp_path):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     recs = [json.loads(x) for x in rep.read_text().splitlines()]
-    assert [x["record"] for x in recs] == ["epoch"] * 4 + ["summary"]
+    assert [x["record"] for x in recs] == ["epoch"] * 4 + ["metrics", "summary"]
     assert recs[-1]["kernel_launches"] > 0
     ctx = Context(0)
     ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
@@ -109,12 +109,26 @@ def test_cli_trains_and_matches_python_host(cli, tmp_path):
     for r in recs[:4]:
         parts = r["t_forward"] + r["t_backward"] + r["t_optimizer"] + r["t_copy"]
         assert r["t_forward"] > 0 and r["t_backward"] > 0 and parts <= r["t_total"] * 1.001 + 1e-6
+    # CorrelationReport per split on the final predictions
+    from scipy import stats
+    yhat = ctx.forward().astype(np.float64)
+    met = recs[4]
+    for code, name in enumerate(("train", "val", "test")):
+        sel = nd.split == code
+        a, b = yhat[sel], nd.labels[sel].astype(np.float64)
+        m = met[name]
+        assert m["count"] == int(sel.sum())
+        assert m["pearson"] == pytest.approx(stats.pearsonr(a, b)[0], abs=1e-6)
+        assert m["spearman"] == pytest.approx(stats.spearmanr(a, b)[0], abs=1e-6)
+        assert m["kendall"] == pytest.approx(stats.kendalltau(a, b)[0], abs=1e-6)
+        assert m["r2"] == pytest.approx(1 - ((b - a) ** 2).sum() / ((b - b.mean()) ** 2).sum(), abs=1e-6)
 
 
 @pytest.mark.gpu
 def test_cli_checkpoint_resume(cli, tmp_path):
-    """--checkpoint writes GSRP of the trained parameters; 2 + 2 epochs
-    with --resume equal 4 epochs except for Adam's moments, which GSRP does not hold."""
+    """--checkpoint writes GSRP of the trained parameters plus the
+    Adam state sidecar (<out>.adam: m, v, step); 2 epochs + --resume 2 epochs
+    equal 4 straight epochs bit for bit."""
     from paper_2603_27156_b200 import MODE_GSRC, Context, init_params, model
     g, nd, gp, np_ = _files(tmp_path, n=2000)
     L, D, C, k = 2, 64, 2, 8
@@ -136,8 +150,17 @@ def test_cli_checkpoint_resume(cli, tmp_path):
     for _ in range(2):
         ctx.train_step(lr=1e-3)
     assert np.array_equal(ctx.params(), q)
-    r = subprocess.run([cli, "train", *args, "--epochs", "1", "--resume", str(ck), "--report", str(tmp_path / "b.jsonl")],
+    m, v, step = ctx.optim_state()
+    raw = (tmp_path / "a.gsrp.adam").read_bytes()
+    assert raw[:4] == b"GSRA" and int(np.frombuffer(raw[16:24], np.int64)[0]) == step == 2
+    assert np.array_equal(np.frombuffer(raw[24:24 + 4 * m.size], np.float32), m)
+    ck2 = tmp_path / "b.gsrp"
+    r = subprocess.run([cli, "train", *args, "--epochs", "2", "--resume", str(ck), "--checkpoint", str(ck2), "--report", str(tmp_path / "b.jsonl")],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
+    assert json.loads((tmp_path / "b.jsonl").read_text().splitlines()[-1])["exact_resume"] is True
+    for _ in range(2):
+        ctx.train_step(lr=1e-3)
+    assert np.array_equal(model.read_gsrp(str(ck2))[0], ctx.params())   # exact resume
     r = subprocess.run([cli, "train", *args[:4], "--hidden", "32", *args[6:], "--epochs", "1", "--resume", str(ck)], capture_output=True, text=True)
     assert r.returncode == 1 and "differs" in r.stderr

@@ -12,7 +12,18 @@
 //       [--layers L] [--hidden D] [--groups C] [--k K] [--epochs E] [--lr LR]
 //       [--norm none|row_mean|sym] [--precision fp32|tf32] [--seed S]
 //       [--params init.f32 | --resume in.gsrp] [--checkpoint out.gsrp]
-//       [--report out.jsonl] [--device I]
+//       [--report out.jsonl] [--device I] [--threads T]
+//       [--nranks N --rank R --comm-file F]
+//
+// After the last epoch a "metrics" record carries the CorrelationReport
+// (Pearson, Spearman, Kendall tau-b, R²) of the predictions
+// per split (train / val / test; test is the SPEC default). --checkpoint also
+// writes the Adam state (m, v, step) to <out>.adam so --resume continues the
+// interrupted trajectory exactly (GSRP itself holds parameters only,
+// SPEC.md:293). Data parallelism: one process per GPU, each with its own graph
+// and node files; rank 0 writes the NCCL id to --comm-file, the others read it,
+// and every step averages the gradients over the ranks.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -22,9 +33,12 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gsr/cuda_api.hpp"
+#include "gsr/metrics.hpp"
+#include "gsr/threads.hpp"
 
 namespace {
 
@@ -69,12 +83,12 @@ Graph read_gsrg(const std::string& path) {
 struct Nodes {
     index_t n = 0, d_in = 0;
     std::vector<float> x, y;
-    std::vector<std::uint8_t> train;
+    std::vector<std::uint8_t> train, split;
     index_t split_count[3] = {0, 0, 0};
 };
 
 // GSRN: "GSRN", u64 n, u64 d_in, f64 features, f64 labels, u8 split.
-Nodes read_gsrn(const std::string& path) {
+Nodes read_gsrn(const std::string& path, gsr::ThreadPool* pool) {
     const auto b = slurp(path);
     if (b.size() < 20 || std::memcmp(b.data(), "GSRN", 4) != 0) throw gsr::FormatError(path + ": bad GSRN magic");
     Nodes d;
@@ -85,10 +99,17 @@ Nodes read_gsrn(const std::string& path) {
     d.x.resize(n * di);
     d.y.resize(n);
     d.train.resize(n);
-    for (size_t i = 0; i < n * di; ++i) d.x[i] = static_cast<float>(get_le<double>(b, 20 + 8 * i));
-    for (size_t i = 0; i < n; ++i) d.y[i] = static_cast<float>(get_le<double>(b, 20 + 8 * n * di + 8 * i));
+    d.split.resize(n);
+    // f64 → f32 decode, row-partitioned over the host pool
+    gsr::parallel_for(pool, d.n, [&](index_t lo, index_t hi) {
+        for (size_t i = static_cast<size_t>(lo); i < static_cast<size_t>(hi); ++i) {
+            for (size_t j = 0; j < di; ++j) d.x[i * di + j] = static_cast<float>(get_le<double>(b, 20 + 8 * (i * di + j)));
+            d.y[i] = static_cast<float>(get_le<double>(b, 20 + 8 * n * di + 8 * i));
+            d.split[i] = static_cast<std::uint8_t>(b[20 + 8 * n * di + 8 * n + i]);
+        }
+    });
     for (size_t i = 0; i < n; ++i) {
-        const auto s = static_cast<std::uint8_t>(b[20 + 8 * n * di + 8 * n + i]);
+        const auto s = d.split[i];
         if (s > 2) throw gsr::FormatError(path + ": split code out of range");
         d.train[i] = s == 0;
         d.split_count[s]++;
@@ -187,11 +208,70 @@ std::vector<float> read_gsrp(const std::string& path, const gsr::cuda::NetConfig
     return p;
 }
 
+// Adam state sidecar <checkpoint>.adam: "GSRA", u32 version 1, u64 P, i64 step,
+// f32 m[P], f32 v[P] (little-endian).
+void write_adam(const std::string& path, const gsr::cuda::Context::OptimState& o) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw gsr::ResourceError("cannot write " + path);
+    const std::uint32_t ver = 1;
+    const std::uint64_t P = o.m.size();
+    const std::int64_t st = o.step;
+    f.write("GSRA", 4);
+    f.write(reinterpret_cast<const char*>(&ver), 4);
+    f.write(reinterpret_cast<const char*>(&P), 8);
+    f.write(reinterpret_cast<const char*>(&st), 8);
+    f.write(reinterpret_cast<const char*>(o.m.data()), static_cast<std::streamsize>(4 * P));
+    f.write(reinterpret_cast<const char*>(o.v.data()), static_cast<std::streamsize>(4 * P));
+}
+
+bool read_adam(const std::string& path, index_t P, gsr::cuda::Context::OptimState& o) {
+    std::ifstream probe(path, std::ios::binary);
+    if (!probe) return false;  // parameters-only checkpoint: a warm start
+    const auto b = slurp(path);
+    if (b.size() < 24 || std::memcmp(b.data(), "GSRA", 4) != 0) throw gsr::FormatError(path + ": bad GSRA magic");
+    if (get_le<std::uint32_t>(b, 4) != 1) throw gsr::FormatError(path + ": unsupported GSRA version");
+    if (get_le<std::uint64_t>(b, 8) != static_cast<std::uint64_t>(P)) throw gsr::ShapeError(path + ": optimizer state size differs from the model");
+    if (b.size() != 24 + 8 * static_cast<size_t>(P)) throw gsr::FormatError(path + ": truncated GSRA");
+    o.step = get_le<std::int64_t>(b, 16);
+    o.m.resize(static_cast<size_t>(P));
+    o.v.resize(static_cast<size_t>(P));
+    std::memcpy(o.m.data(), b.data() + 24, 4 * static_cast<size_t>(P));
+    std::memcpy(o.v.data(), b.data() + 24 + 4 * static_cast<size_t>(P), 4 * static_cast<size_t>(P));
+    return true;
+}
+
+// NCCL id exchange through a file (rank 0 writes it atomically, the others poll).
+std::vector<unsigned char> exchange_comm_id(const std::string& path, int rank) {
+    if (rank == 0) {
+        const auto id = gsr::cuda::Context::comm_unique_id();
+        const std::string tmp = path + ".tmp";
+        {
+            std::ofstream f(tmp, std::ios::binary);
+            if (!f) throw gsr::ResourceError("cannot write " + tmp);
+            f.write(reinterpret_cast<const char*>(id.data()), static_cast<std::streamsize>(id.size()));
+        }
+        if (std::rename(tmp.c_str(), path.c_str()) != 0) throw gsr::ResourceError("cannot publish " + path);
+        return id;
+    }
+    for (int i = 0; i < 1200; ++i) {
+        std::ifstream f(path, std::ios::binary);
+        if (f) {
+            std::vector<unsigned char> id((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+            if (id.size() == 128) return id;
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(50));
+    }
+    throw gsr::ResourceError("no NCCL id in " + path + " after 60 s");
+}
+
+const char* kSplitName[3] = {"train", "val", "test"};
+
 int usage() {
     std::cerr << "usage: gsrnet-cuda train --graph G.gsrg --nodes N.gsrn [--model gsrc|gsr|baseline] [--layers L] [--hidden D]\n"
                  "                        [--groups C] [--k K] [--epochs E] [--lr LR] [--norm none|row_mean|sym]\n"
                  "                        [--precision fp32|tf32] [--seed S] [--params init.f32] [--resume in.gsrp]\n"
-                 "                        [--checkpoint out.gsrp] [--report out.jsonl] [--device I]\n";
+                 "                        [--checkpoint out.gsrp] [--report out.jsonl] [--device I] [--threads T]\n"
+                 "                        [--nranks N --rank R --comm-file F]\n";
     return 1;
 }
 
@@ -236,12 +316,18 @@ int run(int argc, char** argv) {
     gsr::cuda::OptimConfig opt;
     opt.lr = std::stof(get("lr", "1e-3"));
 
+    const int nranks = std::stoi(get("nranks", "1")), rank = std::stoi(get("rank", "0"));
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw gsr::ConfigError("--rank must be in [0, --nranks)");
+    if (nranks > 1 && !a.count("comm-file")) throw gsr::ConfigError("--nranks > 1 needs --comm-file");
+
+    gsr::ThreadPool pool(std::stoi(get("threads", "0")));
     const Graph g = read_gsrg(a["graph"]);
-    const Nodes d = read_gsrn(a["nodes"]);
+    const Nodes d = read_gsrn(a["nodes"], &pool);
     if (d.n != g.n) throw gsr::ShapeError("node file n != graph n");
     c.d_in = static_cast<int>(d.d_in);
 
-    gsr::cuda::Context ctx(std::stoi(get("device", "0")));
+    gsr::cuda::Context ctx(std::stoi(get("device", nranks > 1 ? std::to_string(rank) : "0")));
+    if (nranks > 1) ctx.comm_init(exchange_comm_id(a["comm-file"], rank), nranks, rank);
     ctx.upload_graph(g.n, g.row_ptr, g.col_idx, norm);
     ctx.init_model(c);
     const index_t P = ctx.num_params();
@@ -257,6 +343,14 @@ int run(int argc, char** argv) {
         p = init_params(c, P, std::stoull(get("seed", "0")));
     }
     ctx.set_params(p);
+    bool exact_resume = false;
+    if (a.count("resume")) {  // Adam m, v and step from the sidecar, when the checkpoint has one
+        gsr::cuda::Context::OptimState o;
+        if (read_adam(a["resume"] + ".adam", P, o)) {
+            ctx.set_optim_state(o);
+            exact_resume = true;
+        }
+    }
     ctx.upload_data(d.x.data(), d.y.data(), d.train.data());
     ctx.set_graph_capture(true);
 
@@ -284,7 +378,26 @@ int run(int argc, char** argv) {
           << ",\"utilization\":" << m.utilization << "}\n";
         *out << s.str();
     }
-    if (a.count("checkpoint")) write_gsrp(a["checkpoint"], ctx.params(), c);
+    if (a.count("checkpoint") && rank == 0) {
+        write_gsrp(a["checkpoint"], ctx.params(), c);
+        write_adam(a["checkpoint"] + ".adam", ctx.optim_state());
+    }
+    {  // CorrelationReport per split on the final predictions
+        const std::vector<float> yhat = ctx.forward(g.n);
+        gsr::CorrelationReport cr[3];
+        gsr::parallel_for(&pool, 3, [&](index_t lo, index_t hi) {
+            for (index_t sp = lo; sp < hi; ++sp) cr[sp] = gsr::correlate(yhat.data(), d.y.data(), d.split.data(), g.n, static_cast<int>(sp));
+        });
+        auto num = [](double v) { return std::isfinite(v) ? std::to_string(v) : std::string("null"); };
+        std::ostringstream s;
+        s.precision(9);
+        s << "{\"record\":\"metrics\"";
+        for (int sp = 0; sp < 3; ++sp)
+            s << ",\"" << kSplitName[sp] << "\":{\"count\":" << cr[sp].count << ",\"pearson\":" << num(cr[sp].pearson) << ",\"spearman\":"
+              << num(cr[sp].spearman) << ",\"kendall\":" << num(cr[sp].kendall) << ",\"r2\":" << num(cr[sp].r2) << "}";
+        s << "}\n";
+        *out << s.str();
+    }
     const gsrc_mem_report m = ctx.memory();
     std::ostringstream s;
     s.precision(9);
@@ -292,7 +405,8 @@ int run(int argc, char** argv) {
       << ",\"e\":" << g.col_idx.size() << ",\"layers\":" << c.layers << ",\"hidden\":" << c.hidden << ",\"groups\":" << c.groups
       << ",\"k\":" << c.k << ",\"params\":" << P << ",\"epochs\":" << epochs << ",\"first_loss\":" << first << ",\"last_loss\":" << last
       << ",\"steps_per_s\":" << (epochs > 1 && total > 0 ? (epochs - 1) / total : 0.0) << ",\"peak_active_bytes\":" << m.peak_active_bytes
-      << ",\"kernel_launches\":" << ctx.kernel_launches() << "}\n";
+      << ",\"kernel_launches\":" << ctx.kernel_launches() << ",\"exact_resume\":" << (exact_resume ? "true" : "false")
+      << ",\"nranks\":" << nranks << ",\"rank\":" << rank << ",\"host_threads\":" << pool.size() << "}\n";
     *out << s.str();
     return 0;
 }
