@@ -18,8 +18,10 @@
 //   * FWD / INV (128 threads): thread t owns tile row t end to end. It reads its
 //     row's 8 neighbour slots (Dir::ell, row-addressed), walks its ≤ kSeg
 //     edges (longer "hub" rows come pre-aggregated from k_hub_rows in the
-//     oracle's canonical segment order), accumulates straight into its row of
-//     the UMMA A operand in shared memory (K-major SWIZZLE_128B), scales it,
+//     oracle's canonical segment order), accumulates in its column of a
+//     column-major view of the A buffer (bank = row: a conflict-free scatter
+//     for any indices), then moves the row, scaled, into the UMMA A operand
+//     (K-major SWIZZLE_128B) one 32-column region at a time,
 //     reads its accumulator row back from TMEM (warp w ↔ lane quadrant w), adds
 //     or subtracts the residual row (a TMA tile load into the released A
 //     buffer), and runs its row's GS top-k alone (FWD: the next block's
@@ -144,9 +146,12 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
 // (sc = 1 for unit edges: the multiply is exact). KS = k at compile time
 // (8 or 16), or 0 for any k ≤ 16 with predicated slots. The edge loop is not
 // unrolled (one record in flight ahead): the kernel's code must stay small
-// enough for the instruction cache.
+// enough for the instruction cache. The accumulator is column-major,
+// acc[m·TR + r]: thread r always hits bank r mod 32, so the scatter is
+// conflict-free whatever the indices (a row-major tile costs ~3.5-way
+// conflicts for random columns).
 template <int W, int KS>
-__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv)[kSegF], const float (&sv)[kSegF], int ne, float* Zs, int r) {
+__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv)[kSegF], const float (&sv)[kSegF], int ne, float* acc, int r) {
     const int k = KS ? KS : a.k;
     const int RB = rec_bytes(k), nv4 = (k + 3) >> 2;
     const bool unit = a.dir.unit_edge != 0;
@@ -154,8 +159,7 @@ __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv
     float s1 = sv[1], s2 = sv[2], s3 = sv[3], s4 = sv[4], s5 = sv[5], s6 = sv[6], s7 = sv[7];
     if (ne > 2) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
     if (ne > 3) prefetch_l2(a.rec_in + static_cast<size_t>(c3) * RB);
-    const int rbase = r * 32;
-    const uint32_t rxx = static_cast<uint32_t>((r & 7) << 2) * 0x01010101u;
+    float* col = acc + r;
     float cur_s = sv[0];
     tile::SparseRec cur;
     if (ne > 0) tile::load_rec16(cur, a.rec_in + static_cast<size_t>(cv[0]) * RB, nv4);
@@ -173,21 +177,18 @@ __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv
         const float vv[16] = {cur.v[0].x, cur.v[0].y, cur.v[0].z, cur.v[0].w, cur.v[1].x, cur.v[1].y, cur.v[1].z, cur.v[1].w,
                               cur.v[2].x, cur.v[2].y, cur.v[2].z, cur.v[2].w, cur.v[3].x, cur.v[3].y, cur.v[3].z, cur.v[3].w};
         // a record's k indices are distinct: load all k accumulators, add,
-        // store (no read-after-write chain inside a record). Offsets are
-        // 32-bit shared-window indices; one LOP XOR-swizzles four index bytes
-        // (rx < 32 leaves bit 5, the 32-column region, intact).
+        // store (no read-after-write chain inside a record)
         constexpr int NJ = KS ? KS : 16;
         int off[NJ];
         float old[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            const int xb = static_cast<int>(__byte_perm(iw[j >> 2] ^ rxx, 0u, 0x4440u | static_cast<uint32_t>(j & 3)));  // m ^ rx, m < 64
-            off[j] = rbase + xb + (xb & 32) * (TR - 1);
-            if (KS || j < k) old[j] = Zs[off[j]];
+            off[j] = static_cast<int>(__byte_perm(iw[j >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3))) * TR;
+            if (KS || j < k) old[j] = col[off[j]];
         }
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
-            if (KS || j < k) Zs[off[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
+            if (KS || j < k) col[off[j]] = __fadd_rn(old[j], __fmul_rn(sc, vv[j]));
         cur = nxt;
         cur_s = ns;
     }
@@ -409,33 +410,47 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
             for (int c = 0; c < W; c += 32) tma_prefetch_2d(&a.tm_x, c, row0);
             prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
         }
-        // ---- aggregation into this thread's row of the A operand
+        // ---- aggregation: this thread's row accumulates in column t of the
+        // column-major view acc[m·TR + t] of the A buffer (conflict-free
+        // scatter), then moves, scaled by Â's row factor, into row t of the
+        // K-major SW128 A operand
         {
-            const int rbase = t * 32, rx = (t & 7) << 2;
-#pragma unroll
-            for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(Zs + rbase + ((c ^ rx) & 31) + (c >> 5) * (TR * 32)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            float* acc = Zs;
             float rf = 0.f;
+            int ne = 0;
+            int cv[kSegF];
+            float sv[kSegF];
             if (valid) {
-                int cv[kSegF];
-                float sv[kSegF];
-                const int ne = load_ell_row(a.dir.ell, row, cv, sv);
+                ne = load_ell_row(a.dir.ell, row, cv, sv);
                 rf = __ldg(a.dir.out_f + row);
-                if (ne < 0) {  // hub row: canonical segmented sum precomputed by k_hub_*
-                    const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
-#pragma unroll
-                    for (int c = 0; c < W; c += 4)
-                        if (c < a.ld) *reinterpret_cast<float4*>(Zs + zo(t, c)) = dev::ld4(zh + c);
-                } else {
-                    agg_sparse_row<W, KS>(a, cv, sv, ne, Zs, t);
-                }
             }
-            // Â row scale
+            if (ne >= 0) {
 #pragma unroll
-            for (int c = 0; c < W; c += 4) {
-                float4* p = reinterpret_cast<float4*>(Zs + zo(t, c));
-                float4 v = *p;
-                v.x = __fmul_rn(rf, v.x); v.y = __fmul_rn(rf, v.y); v.z = __fmul_rn(rf, v.z); v.w = __fmul_rn(rf, v.w);
-                *p = v;
+                for (int m = 0; m < W; ++m) acc[m * TR + t] = 0.f;
+                if (ne > 0) agg_sparse_row<W, KS>(a, cv, sv, ne, acc, t);
+            }
+            // columns [h, h + 32) of acc occupy exactly the storage of the A
+            // operand's 32-column region h / 32: one region at a time (32 live
+            // values; a barrier between its reads and its writes)
+            const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
+#pragma unroll
+            for (int h = 0; h < W; h += 32) {
+                float v[32];
+                if (ne < 0) {  // hub row: canonical segmented sum precomputed by k_hub_*
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 z = h + c < a.ld ? dev::ld4(zh + h + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[c] = z.x; v[c + 1] = z.y; v[c + 2] = z.z; v[c + 3] = z.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) v[m] = acc[(h + m) * TR + t];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    *reinterpret_cast<float4*>(Zs + zo(t, h + c)) =
+                        make_float4(__fmul_rn(rf, v[c]), __fmul_rn(rf, v[c + 1]), __fmul_rn(rf, v[c + 2]), __fmul_rn(rf, v[c + 3]));
             }
         }
         tile::fence_proxy_async();
