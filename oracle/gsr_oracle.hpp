@@ -691,12 +691,14 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
             }
         });
         T* Gi = G + i * w;
-        // dW_i = Zᵀ·G_i = (Â·S)ᵀ·G_i. FP32 (and REV) mode evaluates Zᵀ·G_i.
+        // dW_i = Zᵀ·G_i = (Â·S)ᵀ·G_i. FP32 mode evaluates Zᵀ·G_i.
         // TF32 GSR-C mode evaluates the same product as Sᵀ·(Âᵀ·G_i) from the
         // tensor-core operands the device uses (its BIN kernel: S = the
         // block's GS records, Âᵀ·G_i = the aggregation it already holds for the
         // input gradient), both read as TF32 (tf32_op) — see below.
-        const bool tf32_sy = tf32_transform() && !rev && f.use_weight;
+        // (rev-baseline in TF32 likewise, with S = relu(u): the device's BIN in
+        // its dense-mask mode.)
+        const bool tf32_sy = tf32_transform() && f.use_weight;
         if (f.use_weight && !tf32_sy) {
             std::vector<double> acc;
             const bool rz = tf32_transform();
@@ -735,6 +737,10 @@ void rev_backward_layer(Net<T>& net, int l, T* Y, T* G) {
             std::vector<double> acc;
             reduce_outer<T>(n, w, w,
                 [&](index_t r, T* x) {
+                    if (rev) {
+                        for (int j = 0; j < w; ++j) x[j] = static_cast<T>(tf32_op(a.dense[r * w + j]));
+                        return;
+                    }
                     for (int j = 0; j < w; ++j) x[j] = T(0);
                     for (int j = 0; j < k; ++j) x[a.idx[r * k + j]] = static_cast<T>(tf32_op(a.vals[r * k + j]));
                 },

@@ -168,7 +168,9 @@ struct gsrc_ctx {
     int* hcnt_f = nullptr;   // per hub: chunks finished (self-resetting)
     int2* seg_b = nullptr;   // dense hub segments {lo, hi} (launch_hub_dense)
     int *hub_b = nullptr, *segoff_b = nullptr;
-    int nseg_f = 0, nseg_b = 0, nitem_f = 0;
+    int2* seg_fd = nullptr;  // forward-direction dense hub segments (rev-baseline FWD / INV)
+    int *hub_fd = nullptr, *segoff_fd = nullptr;
+    int nseg_f = 0, nseg_b = 0, nitem_f = 0, nseg_fd = 0;
     size_t graph_bytes = 0;
 
     // persistent: model state
@@ -235,6 +237,7 @@ struct gsrc_ctx {
     ~gsrc_ctx() {
         for (cudaGraphExec_t g : {g_fwd, g_bwd, g_opt}) if (g) cudaGraphExecDestroy(g);
         for (void* p : {(void*)rp, (void*)ci, (void*)trp, (void*)tci, (void*)row_f, (void*)col_f, (void*)ell_f, (void*)ell_b, (void*)item_f, (void*)seg_b, (void*)hub_b, (void*)segoff_b,
+                        (void*)seg_fd, (void*)hub_fd, (void*)segoff_fd,
                         (void*)hcnt_f, (void*)params, (void*)grads,
                         (void*)opt_m, (void*)opt_v, (void*)bc, (void*)d_step, (void*)X0, (void*)y, (void*)mask})
             if (p) cudaFree(p);
@@ -351,6 +354,9 @@ struct gsrc_ctx {
     // ---- thread-per-row tcgen05 fast path (fast.cu): GSR-C in TF32 mode ------
     bool no_fast = std::getenv("GSRC_NO_FAST") != nullptr;  // A/B switch: generic k_tile for every block
     bool fast() const { return !no_fast && cfg.mode == GSRC_MODE_GSRC && cfg.gemm == GSRC_GEMM_TF32 && fast_supported(w, k); }
+    // rev-baseline (dense blocks) on the same tcgen05 kernels: dense aggregation of relu(u)
+    bool fast_rev() const { return !no_fast && cfg.mode == GSRC_MODE_REV && cfg.gemm == GSRC_GEMM_TF32 && cfg.use_weight && w <= 64; }
+    bool fastpath() const { return fast() || fast_rev(); }
     FastArgs fast_base(bool transpose) const {
         FastArgs f;
         f.n = static_cast<int>(n);
@@ -373,6 +379,9 @@ struct gsrc_ctx {
             ++launches;
         } else if (!sparse && transpose) {
             CK(launch_hub_dense(f, seg_b, nseg_b, hub_b, segoff_b, nhub_b, Pseg2, st));
+            launches += 2;
+        } else if (!sparse && !transpose) {  // rev-baseline: Â·relu(u) of the forward hub rows into f.Zh
+            CK(launch_hub_dense(f, seg_fd, nseg_fd, hub_fd, segoff_fd, nhub_f, Pseg, st));
             launches += 2;
         } else {
             throw Fail(GSRC_ERR_CONFIG, "hub pre-pass: unsupported direction");
@@ -481,6 +490,62 @@ struct gsrc_ctx {
         }
         run_fast(2, b);
     }
+    // ---- rev-baseline on the fast path ----------------------------------------
+    // f_i(u) = (Â·relu(u))·W_i + b_i with the Eq. 6 add (kind 0) or the Eq. 7
+    // subtract (kind 1): the forward hub rows come from the dense hub pre-pass.
+    void rev_fast_block(int l, int i, const float* u, int kind) {
+        FastArgs f = fast_base(false);
+        f.dense = 1;
+        f.relu = 1;
+        f.x_in = u;
+        run_hub(false, f, false);
+        f.Wm = Wb(l, i);
+        f.bias = Bb(l, i);
+        f.R = plane(X, i);
+        f.out = plane(X, i);
+        f.tm_x = xmaps[static_cast<size_t>(i)];
+        run_fast(kind, f);
+    }
+    // du = (u > 0) ⊙ ((Âᵀ·G_i)·W_iᵀ) into G_{i-1} or every G_j, j ≥ 1; dW_i += relu(u)ᵀ·(Âᵀ·G_i)
+    void rev_fast_input_grad(int l, int i, const float* u, bool hub_done) {
+        FastArgs b = fast_base(true);
+        b.x_in = plane(G, i);
+        b.Zh = Zh2;
+        if (!hub_done) run_hub(false, b, true);
+        b.Wm = Wb(l, i);
+        b.gemm_t = 1;
+        b.mplane = u;
+        b.part = part;
+        if (i > 0) { b.dst[0] = plane(G, i - 1); b.tm_dst[0] = gmaps[static_cast<size_t>(i - 1)]; b.ndst = 1; }
+        else {
+            for (int p = 1; p < C; ++p) { b.dst[p - 1] = plane(G, p); b.tm_dst[p - 1] = gmaps[static_cast<size_t>(p)]; }
+            b.ndst = C - 1;
+        }
+        run_fast(2, b);
+    }
+    // one block of the rev backward sweep: inverse, dW/db and the input gradient
+    void rev_fast_block_backward(int l, int i, const float* u) {
+        const bool side_hub = nhub_b > 0;  // the dense transpose hub rows of G_i beside the forward hub pass and INV
+        if (side_hub) {
+            CK(cudaEventRecord(fork_ev, stream));
+            CK(cudaStreamWaitEvent(side, fork_ev, 0));
+            FastArgs hb = fast_base(true);
+            hb.x_in = plane(G, i);
+            hb.Zh = Zh2;
+            run_hub(false, hb, true, side);
+            CK(cudaEventRecord(join_ev, side));
+        }
+        rev_fast_block(l, i, u, 1);
+        if (side_hub) CK(cudaStreamWaitEvent(stream, join_ev, 0));
+        rev_fast_input_grad(l, i, u, side_hub);
+        reduce_block_grads(l, i);
+        if (cfg.use_bias) {
+            CK(launch_colsum(plane(G, i), static_cast<int>(n), w, ld, part, &last_grid, stream));
+            ++launches;
+            CK(launch_reduce_parts(part, last_grid, w, w, grads + off_block(l, i) + static_cast<size_t>(w) * w, 1, stream));
+            ++launches;
+        }
+    }
 
     // ---- GSR-C / REV layers ---------------------------------------------------
     void rev_layer_forward(int l) {
@@ -489,6 +554,10 @@ struct gsrc_ctx {
         uint8_t* nxt = recB;
         if (sparse) run_gs_groupsum(X, cur);
         else run_sum_planes(X, U);
+        if (fast_rev()) {
+            for (int i = 0; i < C; ++i) rev_fast_block(l, i, i == 0 ? U : plane(X, i - 1), 0);
+            return;
+        }
         if (fast() && cfg.use_weight) {
             for (int i = 0; i < C; ++i) {
                 diag_rec(l, i, cur, 0);
@@ -531,6 +600,11 @@ struct gsrc_ctx {
         } else {
             if (i > 0) u = plane(X, i - 1);
             else { run_sum_planes(X, U); u = U; }
+        }
+        if (fast_rev()) {
+            if (with_grads) rev_fast_block_backward(l, i, u);
+            else rev_fast_block(l, i, u, 1);
+            return;
         }
         if (fast() && cfg.use_weight) {  // the same tensor-core kernels as the forward: an exact inverse on the residual grid
             if (with_grads) fast_block_backward(l, i, recA);
@@ -716,9 +790,9 @@ struct gsrc_ctx {
         total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
         if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
-        if (fast()) total += 2 * bytes_rounded(pl * sizeof(float));        // Zh, Zh2 (hub-row aggregates)
+        if (fastpath()) total += 2 * bytes_rounded(pl * sizeof(float));    // Zh, Zh2 (hub-row aggregates)
         const size_t nsegmax = static_cast<size_t>(std::max(nseg_f, nseg_b));
-        if (fast()) total += 2 * bytes_rounded(std::max<size_t>(nsegmax, 1) * ld * sizeof(float));  // Pseg, Pseg2
+        if (fastpath()) total += 2 * bytes_rounded(std::max<size_t>(nsegmax, 1) * ld * sizeof(float));  // Pseg, Pseg2
         if (alg12) total += 2 * bytes_rounded(pl * sizeof(float)) + 3 * bytes_rounded(rb) + 2 * static_cast<size_t>(cfg.layers) * bytes_rounded(rb);
         arena.plan(total);
         X = arena.lease<float>(pl * C);
@@ -735,13 +809,13 @@ struct gsrc_ctx {
         loss_dev = arena.lease<double>(1);
         U = nullptr;
         if (cfg.mode == GSRC_MODE_REV) U = arena.lease<float>(pl);
-        Zh = fast() ? arena.lease<float>(pl) : nullptr;
-        Pseg = fast() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
-        Zh2 = fast() ? arena.lease<float>(pl) : nullptr;
-        Pseg2 = fast() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
+        Zh = fastpath() ? arena.lease<float>(pl) : nullptr;
+        Pseg = fastpath() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
+        Zh2 = fastpath() ? arena.lease<float>(pl) : nullptr;
+        Pseg2 = fastpath() ? arena.lease<float>(std::max<size_t>(nsegmax, 1) * ld) : nullptr;
         xmaps.assign(static_cast<size_t>(C), CUtensorMap{});
         gmaps.assign(static_cast<size_t>(C), CUtensorMap{});
-        if (fast())
+        if (fastpath())
             for (int p = 0; p < C; ++p) {
                 CK(encode_plane_map(&xmaps[static_cast<size_t>(p)], plane(X, p), static_cast<int>(n), ld));
                 CK(encode_plane_map(&gmaps[static_cast<size_t>(p)], plane(G, p), static_cast<int>(n), ld));
@@ -938,7 +1012,7 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (trp[r + 1] - trp[r] > kAggSeg) hb.push_back(static_cast<int>(r));
         }
         for (void* p : {(void*)ctx->item_f, (void*)ctx->hcnt_f, (void*)ctx->seg_b, (void*)ctx->hub_b, (void*)ctx->segoff_b,
-                        (void*)ctx->ell_f, (void*)ctx->ell_b})
+                        (void*)ctx->seg_fd, (void*)ctx->hub_fd, (void*)ctx->segoff_fd, (void*)ctx->ell_f, (void*)ctx->ell_b})
             if (p) cudaFree(p);
         // per-row neighbour slots (Dir::ell): edge scale = the direction's edge_f of the neighbour
         auto ell_table = [&](const std::vector<int>& ptr, const int* idx, const std::vector<float>& ef) {
@@ -982,23 +1056,26 @@ int gsrc_graph_upload(gsrc_ctx* ctx, int64_t n, int64_t e, const int64_t* row_pt
             if (!hubs.empty()) CK(cudaMemset(cnt, 0, sizeof(int) * hubs.size()));
         };
         hub_table(hf, rp, kHubChunk, ctx->item_f, ctx->nitem_f, ctx->hcnt_f, ctx->nseg_f);
-        {  // dense: flattened segments, per-hub first segment
+        // dense: flattened segments, per-hub first segment (transpose for BIN; forward for the rev-baseline)
+        auto dense_table = [&](const std::vector<int>& hubs, const std::vector<int>& ptr, int2*& seg, int*& segoff, int*& hubrows, int& nseg) {
             std::vector<int2> sv;
-            std::vector<int> ov(hb.size() + 1, 0);
-            for (size_t h = 0; h < hb.size(); ++h) {
+            std::vector<int> ov(hubs.size() + 1, 0);
+            for (size_t h = 0; h < hubs.size(); ++h) {
                 ov[h] = static_cast<int>(sv.size());
-                const int e0 = trp[static_cast<size_t>(hb[h])], e1 = trp[static_cast<size_t>(hb[h]) + 1];
+                const int e0 = ptr[static_cast<size_t>(hubs[h])], e1 = ptr[static_cast<size_t>(hubs[h]) + 1];
                 for (int lo = e0; lo < e1; lo += kAggSeg) sv.push_back(make_int2(lo, std::min(e1, lo + kAggSeg)));
             }
-            ov[hb.size()] = static_cast<int>(sv.size());
-            ctx->nseg_b = static_cast<int>(sv.size());
-            ctx->seg_b = dmalloc<int2>(sv.size(), &ctx->graph_bytes);
-            ctx->segoff_b = dmalloc<int>(ov.size(), &ctx->graph_bytes);
-            ctx->hub_b = dmalloc<int>(hb.size(), &ctx->graph_bytes);
-            if (!sv.empty()) CK(cudaMemcpy(ctx->seg_b, sv.data(), sizeof(int2) * sv.size(), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(ctx->segoff_b, ov.data(), sizeof(int) * ov.size(), cudaMemcpyHostToDevice));
-            if (!hb.empty()) CK(cudaMemcpy(ctx->hub_b, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
-        }
+            ov[hubs.size()] = static_cast<int>(sv.size());
+            nseg = static_cast<int>(sv.size());
+            seg = dmalloc<int2>(sv.size(), &ctx->graph_bytes);
+            segoff = dmalloc<int>(ov.size(), &ctx->graph_bytes);
+            hubrows = dmalloc<int>(hubs.size(), &ctx->graph_bytes);
+            if (!sv.empty()) CK(cudaMemcpy(seg, sv.data(), sizeof(int2) * sv.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(segoff, ov.data(), sizeof(int) * ov.size(), cudaMemcpyHostToDevice));
+            if (!hubs.empty()) CK(cudaMemcpy(hubrows, hubs.data(), sizeof(int) * hubs.size(), cudaMemcpyHostToDevice));
+        };
+        dense_table(hb, trp, ctx->seg_b, ctx->segoff_b, ctx->hub_b, ctx->nseg_b);
+        dense_table(hf, rp, ctx->seg_fd, ctx->segoff_fd, ctx->hub_fd, ctx->nseg_fd);
         CK(cudaDeviceSynchronize());  // pageable copies may still be in flight when cudaMemcpy returns
         const bool resize = ctx->n != n;
         ctx->n = n;

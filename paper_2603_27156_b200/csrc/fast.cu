@@ -210,6 +210,84 @@ __device__ __forceinline__ int load_ell_row(const int2* ell, int row, int (&cv)[
     return cv[0] == -2 ? -1 : ne;  // −1: hub row
 }
 
+// ---- dense row aggregation (rev-baseline FWD / INV) ----------------------
+// Z = Â·relu(x_in) for the tile's rows, the BIN gather scheme: an 8-lane
+// group per row, lane q owning the 16 B column chunks q (and q + 8 at W = 64),
+// so every neighbour-row load is whole 128 B lines; 16 rows per pass. Edges in
+// CSR order from +0 (the oracle's spmm_row order for ≤ kSeg edges); hub rows
+// start from their canonical segmented sum (k_hub_seg_dense + k_hub_fold with
+// relu); then Â's row scale. Rows go straight into the K-major SW128 A operand.
+__device__ __forceinline__ float relu0(float v) { return v > 0.f ? v : 0.f; }  // the oracle's v > 0 ? v : 0 (−0, NaN → +0)
+
+template <int W>
+__device__ __forceinline__ void agg_dense_tile(const FastArgs& a, float* Zs, int row0, int t) {
+    constexpr int NCH = W == 64 ? 2 : 1, LPR = W / 4 / NCH, RPP = TR / LPR, NP = TR / RPP;
+    static_assert(LPR == kSegF, "lane q holds neighbour slot q");
+    const int grp = t / LPR, q = t % LPR;
+    const bool unit = a.dir.unit_edge != 0;
+    int mycv[NP];
+    float myscv[NP], rfv[NP];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {  // every pass's neighbour slots first (row-addressed, no load chain)
+        const int rw = row0 + ps * RPP + grp;
+        int2 e = make_int2(-1, 0);
+        rfv[ps] = 0.f;
+        if (rw < a.n) {
+            e = __ldg(a.dir.ell + static_cast<size_t>(rw) * kSegF + q);
+            rfv[ps] = __ldg(a.dir.out_f + rw);
+        }
+        mycv[ps] = e.x;
+        myscv[ps] = __int_as_float(e.y);
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < NP; ++pass) {
+        const int r = pass * RPP + grp, rw = row0 + r;
+        int myc = -1;
+        float mysc = 1.f, rfr = 0.f;
+#pragma unroll
+        for (int ps = 0; ps < NP; ++ps)
+            if (ps == pass) { myc = mycv[ps]; mysc = myscv[ps]; rfr = rfv[ps]; }
+        const bool hub = __shfl_sync(0xffffffffu, myc, 0, LPR) == -2;
+        float4 acc[NCH];
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hub) {
+            const float* zh = a.Zh + static_cast<size_t>(rw) * a.ld;
+#pragma unroll
+            for (int h = 0; h < NCH; ++h)
+                if (4 * (q + LPR * h) < a.ld) acc[h] = dev::ld4(zh + 4 * (q + LPR * h));
+        }
+        float4 x[kSegF][NCH];
+        bool ok[kSegF];
+#pragma unroll
+        for (int u = 0; u < kSegF; ++u) {
+            const int c = __shfl_sync(0xffffffffu, myc, u, LPR);
+            ok[u] = c >= 0;
+#pragma unroll
+            for (int h = 0; h < NCH; ++h)
+                x[u][h] = (ok[u] && 4 * (q + LPR * h) < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 4 * (q + LPR * h))
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kSegF; ++u) {
+            const float sc = unit ? 1.f : __shfl_sync(0xffffffffu, mysc, u, LPR);
+            if (ok[u]) {
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {
+                    acc[h].x = __fadd_rn(acc[h].x, __fmul_rn(sc, relu0(x[u][h].x)));
+                    acc[h].y = __fadd_rn(acc[h].y, __fmul_rn(sc, relu0(x[u][h].y)));
+                    acc[h].z = __fadd_rn(acc[h].z, __fmul_rn(sc, relu0(x[u][h].z)));
+                    acc[h].w = __fadd_rn(acc[h].w, __fmul_rn(sc, relu0(x[u][h].w)));
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < NCH; ++h)
+            *reinterpret_cast<float4*>(Zs + zo(r, 4 * (q + LPR * h))) =
+                make_float4(__fmul_rn(rfr, acc[h].x), __fmul_rn(rfr, acc[h].y), __fmul_rn(rfr, acc[h].z), __fmul_rn(rfr, acc[h].w));
+    }
+}
+
 // GS top-k of a row held in a swizzled smem tile → CBSR record.
 // Selection: the k largest magnitudes, ties at the threshold T (the k-th
 // largest key) taken lowest column first, columns ascending — the oracle's
@@ -413,8 +491,10 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
         // ---- aggregation: this thread's row accumulates in column t of the
         // column-major view acc[m·TR + t] of the A buffer (conflict-free
         // scatter), then moves, scaled by Â's row factor, into row t of the
-        // K-major SW128 A operand
-        {
+        // K-major SW128 A operand. KS < 0: rev-baseline dense rows.
+        if constexpr (KS < 0) {
+            agg_dense_tile<W>(a, Zs, row0, t);
+        } else {
             float* acc = Zs;
             float rf = 0.f;
             int ne = 0;
@@ -506,7 +586,8 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
             for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Zs + (c >> 5) * (TR * 32), c, row0);
             tma_store_commit();
         }
-        if (a.gs_out && valid) gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+        if constexpr (KS >= 0)
+            if (a.gs_out && valid) gs_row<W, 16>(Zs, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
         if (t == 0) tma_store_wait_read();  // Zs is rewritten by the next tile
         tile::tc_fence_before();
         __syncthreads();
@@ -521,7 +602,9 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
 // edge: an 8-lane group per row makes each neighbour-row load whole 128 B
 // lines; the epilogue gives threads t and t + 128 one column half each of tile
 // row t & 127. The CTA has 8 warps.
-template <int W, int TPR>
+// DM (rev-baseline): S = relu(u) and the mask u > 0 come from the dense row of
+// u (a.mplane) instead of the block's GS record.
+template <int W, int TPR, bool DM>
 __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ FastArgs a) {
     using Pl = Plan<W>;
     constexpr int NT = TPR * TR, HW = W / TPR;  // HW: this thread's epilogue columns
@@ -555,9 +638,17 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
     uint32_t ph0 = 0, ph1 = 0;
     bool dw_pending = false;
     dev::pdl_wait();  // the prologue above touched only W and on-chip state
-    if (tid == 0 && static_cast<int>(blockIdx.x) < n_tiles) {  // the first tile's mask records
-        const int nr = a.n - static_cast<int>(blockIdx.x) * TR < TR ? a.n - static_cast<int>(blockIdx.x) * TR : TR;
-        prefetch_l2_bulk(a.mrec + static_cast<size_t>(blockIdx.x) * TR * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+    // the mask source of a tile: its GS records, or (DM) its rows of u
+    auto mask_span = [&](int ti, const void*& p, uint32_t& bytes) {
+        const int nr = a.n - ti * TR < TR ? a.n - ti * TR : TR;
+        if (DM) { p = a.mplane + static_cast<size_t>(ti) * TR * a.ld; bytes = static_cast<uint32_t>(nr * a.ld * 4); }
+        else { p = a.mrec + static_cast<size_t>(ti) * TR * rec_bytes(a.k_m); bytes = static_cast<uint32_t>(nr * rec_bytes(a.k_m)); }
+    };
+    if (tid == 0 && static_cast<int>(blockIdx.x) < n_tiles) {  // the first tile's mask source
+        const void* p;
+        uint32_t b;
+        mask_span(static_cast<int>(blockIdx.x), p, b);
+        prefetch_l2_bulk(p, b);
     }
 
     for (int tile_i = blockIdx.x; tile_i < n_tiles; tile_i += gridDim.x) {
@@ -574,27 +665,42 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
         if (tid == 0) {  // the next tile's slots and mask records
             prefetch_tile_meta(a.dir, tnext, n_tiles, a.n);
             if (tnext < n_tiles) {
-                const int nr = a.n - tnext * TR < TR ? a.n - tnext * TR : TR;
-                prefetch_l2_bulk(a.mrec + static_cast<size_t>(tnext) * TR * rec_bytes(a.k_m), static_cast<uint32_t>(nr * rec_bytes(a.k_m)));
+                const void* p;
+                uint32_t b;
+                mask_span(tnext, p, b);
+                prefetch_l2_bulk(p, b);
             }
         }
-        // mask record of the row (the block's input records: S and the input-gradient mask)
-        const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
-        uint4 iw4 = make_uint4(0u, 0u, 0u, 0u);
-        if (valid) iw4 = *reinterpret_cast<const uint4*>(rc);
-        const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
-        // ---- S = scatter(V, I) of the row, this thread's columns (BASE32B): dW += Sᵀ·Y
-        // (the previous tile's dW MMA has released S2 / Y2); values loaded only
-        // for this thread's columns (the row's record is in L1 for its threads)
-#pragma unroll
-        for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(S2 + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t hm = 0u;  // this thread's mask columns (mask of a padding / invalid row: empty)
+        if constexpr (DM) {
+            // ---- S = relu(u) and the mask u > 0 from the row of u, this thread's columns (BASE32B)
+            const float* ur = a.mplane + static_cast<size_t>(row) * a.ld;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
-            if (valid && j < a.k_m && c / HW == hf) {
-                S2[zb(t, c)] = *reinterpret_cast<const float*>(rc + 16 + 4 * j);
-                hm |= 1u << (c - c_lo);
+            for (int c = 0; c < HW; c += 4) {
+                const float4 u4 = (valid && c_lo + c < a.ld) ? dev::ld4(ur + c_lo + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float uv[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) hm |= static_cast<uint32_t>(uv[j] > 0.f) << (c + j);
+                *reinterpret_cast<float4*>(S2 + zb(t, c_lo + c)) = make_float4(relu0(u4.x), relu0(u4.y), relu0(u4.z), relu0(u4.w));
+            }
+        } else {
+            // mask record of the row (the block's input records: S and the input-gradient mask)
+            const uint8_t* rc = a.mrec + static_cast<size_t>(row) * rec_bytes(a.k_m);
+            uint4 iw4 = make_uint4(0u, 0u, 0u, 0u);
+            if (valid) iw4 = *reinterpret_cast<const uint4*>(rc);
+            const uint32_t iw[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
+            // ---- S = scatter(V, I) of the row, this thread's columns (BASE32B): dW += Sᵀ·Y
+            // (the previous tile's dW MMA has released S2 / Y2); values loaded only
+            // for this thread's columns (the row's record is in L1 for its threads)
+#pragma unroll
+            for (int c = 0; c < HW; c += 4) *reinterpret_cast<float4*>(S2 + zb(t, c_lo + c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c = static_cast<int>((iw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                if (valid && j < a.k_m && c / HW == hf) {
+                    S2[zb(t, c)] = *reinterpret_cast<const float*>(rc + 16 + 4 * j);
+                    hm |= 1u << (c - c_lo);
+                }
             }
         }
         if (tid == 0) tma_store_wait_read();  // the previous tile's du (Zs) has been read by its reduce-add
@@ -883,6 +989,7 @@ __global__ void __launch_bounds__(256) k_hub_seg_dense(FastArgs a, const int2* _
         for (int q = 0; q < CPL; ++q) {
             const int col = lane + 32 * q;
             x[u][q] = (u < ne && col < a.ld) ? __ldg(a.x_in + static_cast<size_t>(c) * a.ld + col) : 0.f;
+            if (a.relu) x[u][q] = relu0(x[u][q]);
         }
     }
     float acc[CPL];
@@ -1053,7 +1160,7 @@ int occupancy_bin2() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, k_bin2<W, kBinTPR>);
+        cudaFuncGetAttributes(&fa, k_bin2<W, kBinTPR, false>);
         const int by_smem = smem_sm / static_cast<int>(Plan<W>::bytes(BIN) + 1024);
         const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
         const int by_regs = 65536 / (regs * kBinTPR * TR);
@@ -1072,15 +1179,17 @@ cudaError_t launch_bin2(const FastArgs& a, cudaStream_t s, int* grid_out) {
     const int grid = tiles < cap ? tiles : cap;
     if (grid_out) *grid_out = grid;
     if (grid == 0) return cudaSuccess;
-    return launch_pdl(k_bin2<W, kBinTPR>, dim3(grid), dim3(kBinTPR * TR), Plan<W>::bytes(BIN), s, a);
+    if (a.mplane) return launch_pdl(k_bin2<W, kBinTPR, true>, dim3(grid), dim3(kBinTPR * TR), Plan<W>::bytes(BIN), s, a);
+    return launch_pdl(k_bin2<W, kBinTPR, false>, dim3(grid), dim3(kBinTPR * TR), Plan<W>::bytes(BIN), s, a);
 }
 
 template <int W>
 cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {set_attr<W, FWD, 0>(), set_attr<W, FWD, 8>(), set_attr<W, FWD, 16>(), set_attr<W, INV, 0>(), set_attr<W, INV, 8>(),
-                          set_attr<W, INV, 16>(),
-                          cudaFuncSetAttribute(k_bin2<W, kBinTPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
+                          set_attr<W, INV, 16>(), set_attr<W, FWD, -1>(), set_attr<W, INV, -1>(),
+                          cudaFuncSetAttribute(k_bin2<W, kBinTPR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN))),
+                          cudaFuncSetAttribute(k_bin2<W, kBinTPR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(BIN)))})
         if (r != cudaSuccess) e = r;
     return e;
 }
@@ -1089,6 +1198,7 @@ cudaError_t set_attrs() {
 // values), else the predicated any-k variant.
 template <int W, int KIND>
 cudaError_t launch_k(const FastArgs& a, cudaStream_t s, int* g) {
+    if (a.dense) return launch<W, KIND, -1>(a, s, g);
     if (a.k == 16) return launch<W, KIND, 16>(a, s, g);
     if (a.k == 8) return launch<W, KIND, 8>(a, s, g);
     return launch<W, KIND, 0>(a, s, g);
@@ -1140,7 +1250,7 @@ cudaError_t init_fast_attributes() {
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out) {
     if (grid_out) *grid_out = 0;
     if (a.n == 0) return cudaSuccess;
-    if (kind != fast::BIN && (a.k < 1 || a.k > 16)) return cudaErrorInvalidValue;
+    if (kind != fast::BIN && !a.dense && (a.k < 1 || a.k > 16)) return cudaErrorInvalidValue;
     if (a.gs_out && (a.k_gs < 1 || a.k_gs > 16)) return cudaErrorInvalidValue;
     if (a.w <= 32) return fast::launch_w<32>(kind, a, s, grid_out);
     if (a.w <= 64) return fast::launch_w<64>(kind, a, s, grid_out);

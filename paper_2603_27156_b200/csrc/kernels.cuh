@@ -115,6 +115,13 @@ struct FastArgs {
     CUtensorMap tm_x;                      // FWD / INV: 2-D tiled map of the R/out plane (128 rows × 32 cols, SWIZZLE_128B)
     CUtensorMap tm_dst[kMaxDst];           // BIN: maps of the dst planes (TMA reduce-add of the masked gradient tile)
     float qs = 0.f, qi = 0.f;              // FWD / INV: residual-stream grid 2^-s (dev::quant); 0 = off
+    // rev-baseline (dense_block SPEC.md:244-252): FWD / INV aggregate Â·relu(x_in)
+    // (dense rows, ld) instead of records; BIN takes S = relu(u) and the mask
+    // u > 0 from the dense rows of mplane instead of mrec; the dense hub
+    // pre-pass applies relu to its input rows when relu is set
+    int dense = 0;
+    int relu = 0;
+    const float* mplane = nullptr;
 };
 
 bool fast_supported(int w, int k);
