@@ -94,6 +94,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=10)
+    ap.add_argument("--no-depth-sweep", action="store_true", help="skip the peak-HBM depth sweep (L = 20, 80, 200)")
     return ap.parse_args()
 
 
@@ -207,6 +208,36 @@ def cpu_baseline(cfg_name, g, nd, mode_id, threads, samples=1):
             "sample": f"oracle fwd+loss+bwd+Adam at full N={g.n}, E={g.e}: L=1 {t1:.2f}s, L=2 {t2:.2f}s; "
                       f"{L}-layer step extrapolated linearly in L: {step:.1f}s",
             "sample_s": t2, "calibration_s": t1, "extrapolated_step_s": step}
+
+
+def depth_sweep(cfg_name, g, nd, gemm, local, layers=(20, 80, 200)):
+    """Peak HBM vs depth at the config's N (SURVEY.md §8d depth check): one
+    training step at each L; the arena's peak_active and the device-wide
+    cudaMemGetInfo delta must be flat in L (O(N·D) reversible memory)."""
+    import torch
+    from paper_2603_27156_b200 import GEMM_FP32, GEMM_TF32, MODE_GSRC, Context, model
+    _, _, D, C, k = CONFIGS[cfg_name]
+    out = {}
+    for L in layers:
+        torch.cuda.synchronize()
+        free0, _ = torch.cuda.mem_get_info()
+        ctx = Context(local)
+        ctx.graph_upload(g.row_ptr, g.col_idx, norm=1)
+        ctx.model_init(MODE_GSRC, L, D, C, k, 8, gemm=GEMM_TF32 if gemm == "tf32" else GEMM_FP32)
+        ctx.set_params(model.init_params(MODE_GSRC, L, D, C, 8, seed=1))
+        ctx.data_upload(nd.features, nd.labels, nd.train_mask)
+        ctx.set_graph_capture(False)
+        loss = ctx.train_step(lr=LR)
+        torch.cuda.synchronize()
+        free1, _ = torch.cuda.mem_get_info()
+        m = ctx.mem_stats()
+        out[str(L)] = {"arena_peak_active": m["peak_active_bytes"], "arena_reserved": m["reserved_bytes"],
+                       "cudaMemGetInfo_delta": int(free0 - free1), "params": int(ctx.P), "loss": loss}
+        del ctx
+        torch.cuda.synchronize()
+    peaks = [v["arena_peak_active"] for v in out.values()]
+    out["flat"] = max(peaks) - min(peaks) <= 0.01 * max(peaks) + 64 * 1024 * 1024
+    return out
 
 
 def host_threads():
@@ -356,6 +387,10 @@ def run_ours(args):
             v["frac_hbm"] = v["achieved_gbs"] / hbm_peak
             v["share_of_step"] = share[n] / ms_step
 
+    sweep = None
+    if rank == 0 and world == 1 and args.mode == "gsrc" and not args.no_depth_sweep:
+        sweep = depth_sweep(args.config, g, nd, args.gemm, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, g, nd, mode_id, host_threads())
@@ -374,6 +409,7 @@ def run_ours(args):
             "phases_ms_last_step": phases,
             "peak_hbm_bytes": {"arena_peak_active": mem["peak_active_bytes"], "arena_reserved": mem["reserved_bytes"],
                                "cudaMemGetInfo_delta": int(free0 - free1), "utilization": mem["utilization"]},
+            "peak_hbm_depth_sweep": sweep,
             "loss": {"first": losses[0], "last": losses[-1]},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
