@@ -865,6 +865,8 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
 // folds. Work is spread over all SMs regardless of how skewed the hub degrees are.
 // one segment (≤ kSeg records) of a sparse hub row into the private row pr:
 // 128-bit record loads one ahead, two 8-slot halves per record
+// pr = acc + thread: column m of the thread's partial row is pr[m·kHubChunk]
+// (bank = thread: a conflict-free scatter for any indices)
 __device__ __forceinline__ void hub_seg_sparse(const FastArgs& a, int lo, int ne, float* pr) {
     const int k = a.k, RB = rec_bytes(k), nv4 = (k + 3) >> 2;
     const bool unit = a.dir.unit_edge != 0;
@@ -891,7 +893,7 @@ __device__ __forceinline__ void hub_seg_sparse(const FastArgs& a, int lo, int ne
                 float old[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    mm[j] = static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3)));
+                    mm[j] = static_cast<int>(__byte_perm(iw[(h + j) >> 2], 0u, 0x4440u | static_cast<uint32_t>(j & 3))) * kHubChunk;
                     if (h + j < k) old[j] = pr[mm[j]];
                 }
 #pragma unroll
@@ -906,8 +908,11 @@ template <int W>
 __global__ void __launch_bounds__(kHubChunk) k_hub_rows(FastArgs a, const int4* __restrict__ items, int* __restrict__ cnt,
                                                                        float* __restrict__ Pseg) {
     constexpr int PL = W + 4, CH = kHubChunk, NT = CH;
+    // the segment partials accumulate column-major, acc[m·CH + s] (conflict-free
+    // scatter), then move to row-major slot[s·PL + m] for the in-order fold
     __shared__ __align__(16) float slot[CH * PL];
     __shared__ int last;
+    float* acc = slot;
     const int tid = threadIdx.x;
     dev::pdl_wait();
     // work item: {row, first edge, end edge, first segment of the chunk}, {hub index, row's first partial}
@@ -915,12 +920,19 @@ __global__ void __launch_bounds__(kHubChunk) k_hub_rows(FastArgs a, const int4* 
     const int r = ia.x, e0 = ia.y, e1 = ia.z, c0 = ia.w, h = ib.x;
     const int nseg = (e1 - e0 + kSegF - 1) / kSegF;
     const int ns = min(CH, nseg - c0);
-    float* pr = slot + tid * PL;
-#pragma unroll
-    for (int c = 0; c < W; c += 4) *reinterpret_cast<float4*>(pr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int m = 0; m < W; ++m) acc[m * CH + tid] = 0.f;
     if (tid < ns) {
         const int lo = e0 + (c0 + tid) * kSegF;
-        hub_seg_sparse(a, lo, min(kSegF, e1 - lo), pr);
+        hub_seg_sparse(a, lo, min(kSegF, e1 - lo), acc + tid);
+    }
+    {  // column-major → row-major (in place: every value is in registers across the barrier)
+        float v[W];
+#pragma unroll
+        for (int m = 0; m < W; ++m) v[m] = acc[m * CH + tid];
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < W; m += 4) *reinterpret_cast<float4*>(slot + tid * PL + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
     }
     __syncthreads();
     const int ld = a.ld;

@@ -5,9 +5,9 @@
 set -e
 SRC=$1; NAME=$2
 O=paper_2603_27156_b200/csrc/_obj
-cp "$SRC" paper_2603_27156_b200/csrc/_ab_fast.cu
+T=paper_2603_27156_b200/csrc/_ab_fast_$NAME.cu; cp "$SRC" $T
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
-  -c paper_2603_27156_b200/csrc/_ab_fast.cu -o scratch/fast_$NAME.o
-rm -f paper_2603_27156_b200/csrc/_ab_fast.cu
+  -c $T -o scratch/fast_$NAME.o
+rm -f $T
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o scratch/libgsrcuda_$NAME.so $O/kernels.o $O/tile_w32.o $O/tile_w64.o $O/tile_w128.o scratch/fast_$NAME.o $O/capi.o -Xcompiler -fPIC -ldl
 echo scratch/libgsrcuda_$NAME.so
