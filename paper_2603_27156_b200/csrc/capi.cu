@@ -218,6 +218,14 @@ struct gsrc_ctx {
     cudaEvent_t ev[4] = {};
     cudaStream_t side = nullptr;                 // backward sweep: dense hub pre-pass beside the INV
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // backward sweep: the fixed-order dW partial reduction of block i runs on
+    // side2 beside the next block's work; BIN partials alternate between two
+    // buffers, each reused only once its reduction has finished
+    cudaStream_t side2 = nullptr;
+    cudaEvent_t ev_bin[2] = {}, ev_red[2] = {};
+    double* part_bin[2] = {};
+    bool red_pending[2] = {false, false};
+    int part_sel = 0;
     cudaEvent_t tev[4] = {};  // phase marks inside the step (Eq. 9): after forward, after backward, after optimizer, after the all-reduce
     gsrc_timing timing{};
 
@@ -244,11 +252,12 @@ struct gsrc_ctx {
         if (loss_host) cudaFreeHost(loss_host);
         for (auto& e_ : ev) if (e_) cudaEventDestroy(e_);
         for (auto& e_ : tev) if (e_) cudaEventDestroy(e_);
-        for (cudaEvent_t e_ : {fork_ev, join_ev}) if (e_) cudaEventDestroy(e_);
+        for (cudaEvent_t e_ : {fork_ev, join_ev, ev_bin[0], ev_bin[1], ev_red[0], ev_red[1]}) if (e_) cudaEventDestroy(e_);
         if (diag_store) cudaFree(diag_store);
         if (diag_cnt) cudaFree(diag_cnt);
         if (comm) nccl_api().comm_destroy(comm);
         if (side) cudaStreamDestroy(side);
+        if (side2) cudaStreamDestroy(side2);
         if (own) cudaStreamDestroy(own);
     }
 
@@ -333,12 +342,22 @@ struct gsrc_ctx {
         CK(launch_sum_planes(g, out, stream));
         ++launches;
     }
-    void reduce_block_grads(int l, int i) {
+    void reduce_block_grads(int l, int i, const double* src = nullptr, cudaStream_t s_ = nullptr) {
         const int plen = w * w + w;
         float* dst = grads + off_block(l, i);
-        if (cfg.use_weight) CK(launch_reduce_parts(part, last_grid, plen, plen, dst, 1, stream));
-        else CK(launch_reduce_parts(part + static_cast<size_t>(w) * w, last_grid, plen, w, dst + static_cast<size_t>(w) * w, 1, stream));
+        const double* pp = src ? src : part;
+        cudaStream_t st = s_ ? s_ : stream;
+        if (cfg.use_weight) CK(launch_reduce_parts(pp, last_grid, plen, plen, dst, 1, st));
+        else CK(launch_reduce_parts(pp + static_cast<size_t>(w) * w, last_grid, plen, w, dst + static_cast<size_t>(w) * w, 1, st));
         ++launches;
+    }
+    // join side2: every pending dW reduction of the sweep is complete on `stream`
+    void join_reductions() {
+        for (int b = 0; b < 2; ++b)
+            if (red_pending[b]) {
+                CK(cudaStreamWaitEvent(stream, ev_red[b], 0));
+                red_pending[b] = false;
+            }
     }
 
     // mask-flip diagnostic: mode 0 stores the forward masks of block i of layer
@@ -461,8 +480,17 @@ struct gsrc_ctx {
             diag_rec(l, i, rec, 1);
             fast_inverse(l, i, rec, own);
             if (side_hub) CK(cudaStreamWaitEvent(stream, join_ev, 0));
-            fast_input_grad(l, i, rec, side_hub);
-            reduce_block_grads(l, i);
+            // BIN into part_bin[b] once that buffer's previous reduction is done;
+            // its own reduction then runs on side2 beside the next block
+            const int b = part_sel;
+            part_sel ^= 1;
+            if (red_pending[b]) CK(cudaStreamWaitEvent(stream, ev_red[b], 0));
+            fast_input_grad(l, i, rec, side_hub, part_bin[b]);
+            CK(cudaEventRecord(ev_bin[b], stream));
+            CK(cudaStreamWaitEvent(side2, ev_bin[b], 0));
+            reduce_block_grads(l, i, part_bin[b], side2);
+            CK(cudaEventRecord(ev_red[b], side2));
+            red_pending[b] = true;
             if (cfg.use_bias) {
                 CK(launch_colsum(plane(G, i), static_cast<int>(n), w, ld, part, &last_grid, stream));
                 ++launches;
@@ -473,7 +501,7 @@ struct gsrc_ctx {
     }
     bool fast_sweep() const { return fast() && cfg.use_weight && cfg.mode == GSRC_MODE_GSRC && C >= 2; }
     // hub_done: the dense hub pre-pass into Zh2 was already enqueued (side stream)
-    void fast_input_grad(int l, int i, const uint8_t* rec, bool hub_done = false) {
+    void fast_input_grad(int l, int i, const uint8_t* rec, bool hub_done = false, double* bin_part = nullptr) {
         FastArgs b = fast_base(true);
         b.x_in = plane(G, i);
         b.Zh = Zh2;
@@ -482,7 +510,7 @@ struct gsrc_ctx {
         b.gemm_t = 1;
         b.mrec = rec;
         b.k_m = k;
-        b.part = part;
+        b.part = bin_part ? bin_part : part;
         if (i > 0) { b.dst[0] = plane(G, i - 1); b.tm_dst[0] = gmaps[static_cast<size_t>(i - 1)]; b.ndst = 1; }
         else {
             for (int p = 1; p < C; ++p) { b.dst[p - 1] = plane(G, p); b.tm_dst[p - 1] = gmaps[static_cast<size_t>(p)]; }
@@ -644,7 +672,11 @@ struct gsrc_ctx {
     }
     void rev_layer_inverse(int l) { for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, false); }
     void rev_layer_backward(int l) {
-        if (fast_sweep()) { fast_layer_backward(l, false, false); return; }
+        if (fast_sweep()) {
+            fast_layer_backward(l, false, false);
+            join_reductions();
+            return;
+        }
         for (int i = C - 1; i >= 0; --i) rev_block_inverse(l, i, true);
     }
 
@@ -733,6 +765,7 @@ struct gsrc_ctx {
             if (fast_sweep()) fast_layer_backward(l, l < cfg.layers - 1, l > 0);
             else layer_backward(l);
         }
+        join_reductions();
         const int elen = cfg.d_in * cfg.hidden + cfg.hidden;
         CK(launch_encoder_bwd(X0, G, static_cast<int>(n), cfg.d_in, cfg.hidden, C, w, ld, part, nparts_small, stream));
         ++launches;
@@ -787,6 +820,8 @@ struct gsrc_ctx {
         total += 2 * bytes_rounded(rb);                                    // recA, recB
         if (fast() && C > 2) total += static_cast<size_t>(C - 2) * bytes_rounded(rb);  // rblk[2..C-1]
         total += bytes_rounded(part_len * sizeof(double));
+        const size_t bin_part_len = static_cast<size_t>(fast_bin_grid_max()) * plen;
+        if (fast_sweep()) total += 2 * bytes_rounded(bin_part_len * sizeof(double));  // part_bin[0..1]
         total += 2 * bytes_rounded(static_cast<size_t>(n) * sizeof(float));  // yhat, gy
         total += bytes_rounded(static_cast<size_t>(loss_nparts) * sizeof(double)) + 256;
         if (cfg.mode == GSRC_MODE_REV) total += bytes_rounded(pl * sizeof(float));
@@ -803,6 +838,9 @@ struct gsrc_ctx {
         if (fast())
             for (int i = 2; i < C; ++i) rblk.push_back(arena.lease<uint8_t>(rb));
         part = arena.lease<double>(part_len);
+        part_bin[0] = part_bin[1] = nullptr;
+        if (fast_sweep())
+            for (auto& pb_ : part_bin) pb_ = arena.lease<double>(bin_part_len);
         yhat = arena.lease<float>(static_cast<size_t>(n));
         gy = arena.lease<float>(static_cast<size_t>(n));
         loss_part = arena.lease<double>(static_cast<size_t>(loss_nparts));
@@ -933,6 +971,11 @@ int gsrc_create(int device, gsrc_ctx** out) {
     if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
+    if (cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
+    for (int b = 0; b < 2; ++b) {
+        cudaEventCreateWithFlags(&ctx->ev_bin[b], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ctx->ev_red[b], cudaEventDisableTiming);
+    }
     if (init_kernel_attributes() != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     if (cudaMallocHost(&ctx->loss_host, sizeof(double)) != cudaSuccess) { delete ctx; return GSRC_ERR_RESOURCE; }
     *out = ctx;

@@ -43,6 +43,8 @@
 // truncates the same operands.
 #include "tile.cuh"
 
+#include <cstdlib>
+
 namespace gsrk {
 namespace fast {
 
@@ -150,19 +152,47 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
 // acc[m·TR + r]: thread r always hits bank r mod 32, so the scatter is
 // conflict-free whatever the indices (a row-major tile costs ~3.5-way
 // conflicts for random columns).
-template <int W, int KS>
-__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv)[kSegF], const float (&sv)[kSegF], int ne, float* acc, int r) {
+// Record window (k_fws): the records of rows [wlo, wlo + wcnt) staged in
+// shared memory by one bulk copy; a neighbour inside it is read from there
+// (generic loads), any other from global memory.
+struct RecWin {
+    const uint8_t* p = nullptr;
+    int lo = 0, cnt = 0;
+};
+__device__ __forceinline__ void load_rec_any(tile::SparseRec& r, const uint8_t* rc, int nv4) {
+    r.idx = *reinterpret_cast<const uint4*>(rc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r.v[q] = q < nv4 ? *reinterpret_cast<const float4*>(rc + 16 + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+template <bool WIN>
+__device__ __forceinline__ const uint8_t* rec_src(const FastArgs& a, const RecWin& w, int c, int RB, bool& local) {
+    if constexpr (WIN) {
+        local = static_cast<unsigned>(c - w.lo) < static_cast<unsigned>(w.cnt);
+        return local ? w.p + (c - w.lo) * RB : a.rec_in + static_cast<size_t>(c) * RB;
+    } else {
+        local = false;
+        return a.rec_in + static_cast<size_t>(c) * RB;
+    }
+}
+
+template <int W, int KS, bool WIN = false>
+__device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv)[kSegF], const float (&sv)[kSegF], int ne, float* acc, int r,
+                                               const RecWin& win = RecWin{}) {
     const int k = KS ? KS : a.k;
     const int RB = rec_bytes(k), nv4 = (k + 3) >> 2;
     const bool unit = a.dir.unit_edge != 0;
     int c1 = cv[1], c2 = cv[2], c3 = cv[3], c4 = cv[4], c5 = cv[5], c6 = cv[6], c7 = cv[7];
     float s1 = sv[1], s2 = sv[2], s3 = sv[3], s4 = sv[4], s5 = sv[5], s6 = sv[6], s7 = sv[7];
-    if (ne > 2) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
-    if (ne > 3) prefetch_l2(a.rec_in + static_cast<size_t>(c3) * RB);
+    bool loc;
+    if (ne > 2) { const uint8_t* q2 = rec_src<WIN>(a, win, c2, RB, loc); if (!loc) prefetch_l2(q2); }
+    if (ne > 3) { const uint8_t* q3 = rec_src<WIN>(a, win, c3, RB, loc); if (!loc) prefetch_l2(q3); }
     float* col = acc + r;
     float cur_s = sv[0];
     tile::SparseRec cur;
-    if (ne > 0) tile::load_rec16(cur, a.rec_in + static_cast<size_t>(cv[0]) * RB, nv4);
+    if (ne > 0) {
+        if constexpr (WIN) load_rec_any(cur, rec_src<WIN>(a, win, cv[0], RB, loc), nv4);
+        else tile::load_rec16(cur, a.rec_in + static_cast<size_t>(cv[0]) * RB, nv4);
+    }
 #pragma unroll 1
     for (int u = 0; u < ne; ++u) {
         const int nc = c1;  // shift registers of the remaining neighbour ids / scales
@@ -170,8 +200,11 @@ __device__ __forceinline__ void agg_sparse_row(const FastArgs& a, const int (&cv
         c1 = c2; c2 = c3; c3 = c4; c4 = c5; c5 = c6; c6 = c7;
         s1 = s2; s2 = s3; s3 = s4; s4 = s5; s5 = s6; s6 = s7;
         tile::SparseRec nxt = cur;
-        if (u + 1 < ne) tile::load_rec16(nxt, a.rec_in + static_cast<size_t>(nc) * RB, nv4);
-        if (u + 3 < ne) prefetch_l2(a.rec_in + static_cast<size_t>(c2) * RB);
+        if (u + 1 < ne) {
+            if constexpr (WIN) load_rec_any(nxt, rec_src<WIN>(a, win, nc, RB, loc), nv4);
+            else tile::load_rec16(nxt, a.rec_in + static_cast<size_t>(nc) * RB, nv4);
+        }
+        if (u + 3 < ne) { const uint8_t* q2 = rec_src<WIN>(a, win, c2, RB, loc); if (!loc) prefetch_l2(q2); }
         const float sc = unit ? 1.f : cur_s;
         const uint32_t iw[4] = {cur.idx.x, cur.idx.y, cur.idx.z, cur.idx.w};
         const float vv[16] = {cur.v[0].x, cur.v[0].y, cur.v[0].z, cur.v[0].w, cur.v[1].x, cur.v[1].y, cur.v[1].z, cur.v[1].w,
@@ -597,6 +630,230 @@ __global__ void __launch_bounds__(TR, 4) k_fast(const __grid_constant__ FastArgs
     if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
 }
 
+// ---- warp-specialised FWD / INV (sparse records) ----------------------------
+// k_fast runs every phase of a tile on the same 128 threads: its record
+// gathers (a chain of dependent L2/DRAM latencies per row) and its GS top-k
+// selection (ALU-bound, ~1.1k instructions per row) never overlap (ncu, c3:
+// 0.27 vs 0.22 ms per launch with / without the GS epilogue). Here the CTA has
+// two warp groups:
+//   * warps 0-3 (aggregation; thread t = tile row t): tile j's sparse
+//     aggregation into the A operand Zs — the k_fast arithmetic — reading
+//     neighbour records from a shared-memory window of the records of rows
+//     [row0 − kWinH, row0 + TR + kWinH) (one bulk copy, issued a tile ahead,
+//     double-buffered) and from global memory outside it; thread 0 then issues
+//     the MMA into TMEM accumulator j & 1;
+//   * warps 4-7 (epilogue; thread e = tile row e, warp ↔ TMEM lane quadrant
+//     warp & 3): tile j − 1 meanwhile — accumulator row + bias, residual grid,
+//     ± the residual row (TMA-loaded into Out), TMA store, then the GS top-k of
+//     the output row (the next block's records).
+// Handshakes: mbarriers mma_done[b] (tcgen05.commit: accumulator b full, and
+// Zs free again), res_full (the residual tile is in Out), acc_free[b] (the 128
+// epilogue threads have drained accumulator b), win_full[b] (record window
+// b); named barriers 1 / 2 keep each group's own phases apart.
+constexpr int kWinH = 16;  // record-window halo rows on each side of a tile
+
+template <int W>
+struct PlanWs {
+    static constexpr int tile = TR * W;
+    static constexpr int win = (TR + 2 * kWinH) * 80 / 4;  // floats per window (records ≤ 80 B)
+    static constexpr int floats = W * W + 2 * tile + 2 * win;  // Ws | Zs | Out | Win[0] | Win[1]
+    static constexpr size_t bytes = static_cast<size_t>(floats + 64) * sizeof(float);
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int W, int KIND, int KS>
+__global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastArgs a) {
+    static_assert((KIND == FWD || KIND == INV) && KS >= 0, "sparse FWD / INV");
+    using Pl = PlanWs<W>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* base = reinterpret_cast<float*>(smem_raw);
+    if ((smem_u32(base) & 1023u) != 0) __trap();
+    float* Ws = base;
+    float* Zs = Ws + W * W;
+    float* Ob = Zs + Pl::tile;
+    uint8_t* Win = reinterpret_cast<uint8_t*>(Ob + Pl::tile);  // Win[b] = Win + b·Pl::win·4
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Pl::floats);  // mma_done[2] | acc_free[2] | win_full[2] | res_full
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
+    const int tid = threadIdx.x, wid = tid >> 5, t = tid & (TR - 1);
+    const int n_tiles = (a.n + TR - 1) / TR;
+    const int my_tiles = static_cast<int>(blockIdx.x) < n_tiles ? (n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+    constexpr uint32_t TCOLS = 2 * W < 32 ? 32 : 2 * W;  // two accumulators
+    const int RB = rec_bytes(KS ? KS : a.k);
+
+    for (int i = tid; i < W * W; i += 2 * TR) {  // transform operand Bᵀ[n][m] (K-major SW128)
+        const int r = i / W, c = i % W;
+        float v = 0.f;
+        if (r < a.w && c < a.w) v = a.gemm_t ? a.Wm[c * a.w + r] : a.Wm[r * a.w + c];
+        Ws[tile::boff<W>(c, r)] = v;
+    }
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) { mbar_init(&bar[b], 1); mbar_init(&bar[2 + b], TR); mbar_init(&bar[4 + b], 1); }
+        mbar_init(&bar[6], 1);
+    }
+    if (wid == 0) tile::tmem_alloc(tslot, TCOLS);
+    tile::fence_proxy_async();
+    tile::tc_fence_before();
+    __syncthreads();
+    tile::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    dev::pdl_wait();  // the prologue above touched only W and on-chip state
+
+    auto tile_of = [&](int jj) { return static_cast<int>(blockIdx.x) + jj * static_cast<int>(gridDim.x); };
+    if (tid < TR) {
+        // ================= aggregation group (warps 0-3) =================
+        auto win_span = [&](int jj, int& lo, int& cnt) {
+            const int r0 = tile_of(jj) * TR;
+            lo = r0 - kWinH > 0 ? r0 - kWinH : 0;
+            const int hi = r0 + TR + kWinH < a.n ? r0 + TR + kWinH : a.n;
+            cnt = hi - lo;
+        };
+        auto issue_win = [&](int jj) {  // records of tile jj's window → Win[jj & 1]
+            int lo, cnt;
+            win_span(jj, lo, cnt);
+            uint64_t* wb = &bar[4 + (jj & 1)];
+            mbar_expect_tx(wb, static_cast<uint32_t>(cnt * RB));
+            bulk_load(Win + (jj & 1) * (Pl::win * 4), a.rec_in + static_cast<size_t>(lo) * RB, static_cast<uint32_t>(cnt * RB), wb);
+        };
+        if (t == 0 && my_tiles > 0) issue_win(0);
+        for (int j = 0; j < my_tiles; ++j) {
+            const int tile_i = tile_of(j);
+            const int row0 = tile_i * TR, row = row0 + t;
+            const bool valid = row < a.n;
+            const int b = j & 1;
+            if (KIND == INV && j == my_tiles - 1) dev::pdl_trigger();
+            if (t == 0) {
+                prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
+                if (j + 1 < my_tiles) {  // Win[(j + 1) & 1] was last read by tile j − 1 (before its barriers)
+                    tile::fence_proxy_async();
+                    issue_win(j + 1);
+                }
+            }
+            float rf = 0.f;
+            int ne = 0;
+            int cv[kSegF];
+            float sv[kSegF];
+            if (valid) {
+                ne = load_ell_row(a.dir.ell, row, cv, sv);
+                rf = __ldg(a.dir.out_f + row);
+            }
+            RecWin wn;
+            win_span(j, wn.lo, wn.cnt);
+            wn.p = Win + b * (Pl::win * 4);
+            mbar_wait(&bar[4 + b], static_cast<uint32_t>(j >> 1) & 1u);  // window j is in
+            if (j > 0) mbar_wait(&bar[(j - 1) & 1], static_cast<uint32_t>((j - 1) >> 1) & 1u);  // MMA j − 1 has read Zs
+            float* acc = Zs;
+            if (ne >= 0) {
+#pragma unroll
+                for (int m = 0; m < W; ++m) acc[m * TR + t] = 0.f;
+                if (ne > 0) agg_sparse_row<W, KS, true>(a, cv, sv, ne, acc, t, wn);
+            }
+            const float* zh = a.Zh + static_cast<size_t>(row) * a.ld;
+#pragma unroll
+            for (int h = 0; h < W; h += 32) {
+                float v[32];
+                if (ne < 0) {  // hub row: canonical segmented sum precomputed by k_hub_rows
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 z = h + c < a.ld ? dev::ld4(zh + h + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[c] = z.x; v[c + 1] = z.y; v[c + 2] = z.z; v[c + 3] = z.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) v[m] = acc[(h + m) * TR + t];
+                }
+                named_bar_sync(1, TR);
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    *reinterpret_cast<float4*>(Zs + zo(t, h + c)) =
+                        make_float4(__fmul_rn(rf, v[c]), __fmul_rn(rf, v[c + 1]), __fmul_rn(rf, v[c + 2]), __fmul_rn(rf, v[c + 3]));
+            }
+            tile::fence_proxy_async();
+            named_bar_sync(1, TR);
+            if (t == 0) {
+                if (j >= 2) mbar_wait(&bar[2 + b], static_cast<uint32_t>((j >> 1) - 1) & 1u);  // tile j − 2 has left accumulator b
+                tile::tc_fence_after();
+                const uint32_t za = smem_u32(Zs), wa = smem_u32(Ws);
+#pragma unroll
+                for (int kk = 0; kk < W / 8; ++kk)
+                    umma(tmem + static_cast<uint32_t>(b * W), desc_sw128(za + (kk >> 2) * (TR * 128) + (kk & 3) * 32, 16),
+                         desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16), idesc<W>(0, 0), kk > 0 ? 1u : 0u);
+                tile::umma_commit(&bar[b]);
+            }
+        }
+    } else {
+        // ================= epilogue group (warps 4-7) =================
+        const uint32_t tlane = static_cast<uint32_t>(32 * (wid & 3)) << 16;
+        auto issue_res = [&](int jj) {  // residual tile jj → Out (rows ≥ n read as 0)
+            mbar_expect_tx(&bar[6], static_cast<uint32_t>(TR * W * 4));
+#pragma unroll
+            for (int c = 0; c < W; c += 32) tma_load_2d(&a.tm_x, Ob + (c >> 5) * (TR * 32), &bar[6], c, tile_of(jj) * TR);
+        };
+        if (t == 0 && my_tiles > 0) issue_res(0);
+        for (int j = 0; j < my_tiles; ++j) {
+            const int row0 = tile_of(j) * TR, row = row0 + t;
+            const bool valid = row < a.n;
+            const int b = j & 1;
+            if (t == 0 && j + 1 < my_tiles) {
+#pragma unroll
+                for (int c = 0; c < W; c += 32) tma_prefetch_2d(&a.tm_x, c, tile_of(j + 1) * TR);
+            }
+            mbar_wait(&bar[b], static_cast<uint32_t>(j >> 1) & 1u);  // accumulator b holds tile j
+            tile::tc_fence_after();
+            mbar_wait(&bar[6], static_cast<uint32_t>(j) & 1u);  // residual tile j is in Out
+#pragma unroll
+            for (int c0 = 0; c0 < W; c0 += 16) {
+                float h[16];
+                tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(b * W + c0), h);
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                    const int c = c0 + q;
+                    float o[4];
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        float hv = h[q + jj];
+                        if (a.bias) hv = __fadd_rn(hv, c + jj < a.w ? __ldg(a.bias + c + jj) : 0.f);
+                        o[jj] = dev::quant(hv, a.qs, a.qi);
+                    }
+                    float4* rp = reinterpret_cast<float4*>(Ob + zo(t, c));
+                    const float4 R = *rp;
+                    if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
+                    else { o[0] = __fsub_rn(R.x, o[0]); o[1] = __fsub_rn(R.y, o[1]); o[2] = __fsub_rn(R.z, o[2]); o[3] = __fsub_rn(R.w, o[3]); }
+                    *rp = make_float4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            tile::tc_fence_before();
+            mbar_arrive(&bar[2 + b]);  // accumulator b drained
+            tile::fence_proxy_async();
+            named_bar_sync(2, TR);
+            if (t == 0) {
+#pragma unroll
+                for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Ob + (c >> 5) * (TR * 32), c, row0);
+                tma_store_commit();
+            }
+            if (a.gs_out && valid) gs_row<W, 16>(Ob, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+            named_bar_sync(2, TR);  // every read of Out is done
+            if (t == 0) {
+                tma_store_wait_read();
+                if (j + 1 < my_tiles) {
+                    tile::fence_proxy_async();
+                    issue_res(j + 1);
+                }
+            }
+        }
+    }
+    tile::tc_fence_before();
+    __syncthreads();
+    if (wid == 0) tile::tmem_dealloc(tmem, TCOLS);
+}
+
 // ---- BIN: input gradient and dW, two threads per row ------------------------
 // The dense transposed aggregation gathers a full neighbour row (4w bytes) per
 // edge: an 8-lane group per row makes each neighbour-row load whole 128 B
@@ -712,6 +969,7 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
         {
             constexpr int NCH = (TPR == 2 && W == 64) ? 2 : 1;  // 16 B chunks per lane: columns 4q (+4·LPR)
             constexpr int LPR = W / 4 / NCH;                    // lanes per row
+            static_assert(LPR == kSegF, "lane q of a row's group holds neighbour slot q");
             constexpr int RPP = NT / LPR;                       // rows per pass
             constexpr int NP = TR / RPP;                        // passes
             const int grp = tid / LPR, q = tid % LPR;
@@ -750,20 +1008,32 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
                     for (int h = 0; h < NCH; ++h)
                         if (4 * (q + LPR * h) < a.ld) acc[h] = dev::ld4(zh + 4 * (q + LPR * h));
                 }
-                // every lane runs the shuffles (whole-warp masks); rows differ only in predicates
+                // every lane runs the shuffles (whole-warp masks); rows differ only in
+                // predicates. Slots are filled in CSR order (−1 after the last edge), so
+                // the warp walks only as many slots as its longest row has edges.
+                int nmax = 0;
+                {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, myc >= 0);
+#pragma unroll
+                    for (int g = 0; g < 32 / LPR; ++g) nmax = max(nmax, __popc((bal >> (g * LPR)) & 0xffu));
+                }
                 float4 x[kSegF][NCH];
                 bool ok[kSegF];
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
-                    const int c = __shfl_sync(0xffffffffu, myc, u, LPR);
-                    ok[u] = c >= 0;  // slots are filled in CSR order, −1 after the last edge
+                    ok[u] = false;
+                    if (u < nmax) {
+                        const int c = __shfl_sync(0xffffffffu, myc, u, LPR);
+                        ok[u] = c >= 0;
 #pragma unroll
-                    for (int h = 0; h < NCH; ++h)
-                        x[u][h] = (ok[u] && 4 * (q + LPR * h) < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 4 * (q + LPR * h))
-                                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int h = 0; h < NCH; ++h)
+                            x[u][h] = (ok[u] && 4 * (q + LPR * h) < a.ld) ? dev::ld4(a.x_in + static_cast<size_t>(c) * a.ld + 4 * (q + LPR * h))
+                                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < kSegF; ++u) {
+                    if (u >= nmax) break;
                     const float sc = unit ? 1.f : __shfl_sync(0xffffffffu, mysc, u, LPR);
                     if (ok[u]) {
 #pragma unroll
@@ -1158,8 +1428,46 @@ cudaError_t launch(const FastArgs& a, cudaStream_t s, int* grid_out) {
 }
 
 template <int W, int KIND, int KS>
+int occupancy_ws() {
+    static int occ = 0;
+    if (!occ) {
+        int dev = 0, smem_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k_fws<W, KIND, KS>);
+        const int by_smem = smem_sm / static_cast<int>(PlanWs<W>::bytes + 1024);
+        const int regs = fa.numRegs > 0 ? ((fa.numRegs + 7) & ~7) : 255;
+        const int by_regs = 65536 / (regs * 2 * TR);
+        constexpr int tcols = 2 * W < 32 ? 32 : 2 * W;
+        occ = by_smem < by_regs ? by_smem : by_regs;
+        if (occ > 512 / tcols) occ = 512 / tcols;
+        if (occ < 1) occ = 1;
+    }
+    return occ;
+}
+
+bool use_ws() {
+    static const int v = std::getenv("GSRC_NO_WS") ? 0 : 1;  // A/B switch: the single-group k_fast
+    return v != 0;
+}
+
+template <int W, int KIND, int KS>
+cudaError_t launch_ws(const FastArgs& a, cudaStream_t s, int* grid_out) {
+    const int tiles = (a.n + TR - 1) / TR;
+    const int cap = tile::sm_count_host() * occupancy_ws<W, KIND, KS>();
+    const int grid = tiles < cap ? tiles : cap;
+    if (grid_out) *grid_out = grid;
+    if (grid == 0) return cudaSuccess;
+    return launch_pdl(k_fws<W, KIND, KS>, dim3(grid), dim3(2 * TR), PlanWs<W>::bytes, s, a);
+}
+
+template <int W, int KIND, int KS>
 cudaError_t set_attr() {
-    return cudaFuncSetAttribute(k_fast<W, KIND, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(KIND)));
+    cudaError_t e = cudaFuncSetAttribute(k_fast<W, KIND, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Plan<W>::bytes(KIND)));
+    if constexpr (KS >= 0)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fws<W, KIND, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(PlanWs<W>::bytes));
+    return e;
 }
 
 constexpr int kBinTPR = 2;  // BIN threads per tile row (epilogue columns W / kBinTPR each)
@@ -1211,6 +1519,11 @@ cudaError_t set_attrs() {
 template <int W, int KIND>
 cudaError_t launch_k(const FastArgs& a, cudaStream_t s, int* g) {
     if (a.dense) return launch<W, KIND, -1>(a, s, g);
+    if (use_ws()) {
+        if (a.k == 16) return launch_ws<W, KIND, 16>(a, s, g);
+        if (a.k == 8) return launch_ws<W, KIND, 8>(a, s, g);
+        return launch_ws<W, KIND, 0>(a, s, g);
+    }
     if (a.k == 16) return launch<W, KIND, 16>(a, s, g);
     if (a.k == 8) return launch<W, KIND, 8>(a, s, g);
     return launch<W, KIND, 0>(a, s, g);
@@ -1257,6 +1570,11 @@ cudaError_t init_fast_attributes() {
                           cudaFuncSetAttribute(fast::k_gs_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * fast::TR * 64 * 4 + 64)})
         if (r != cudaSuccess) e = r;
     return e;
+}
+
+int fast_bin_grid_max() {
+    const int a = fast::occupancy_bin2<32>(), b = fast::occupancy_bin2<64>();
+    return tile::sm_count_host() * (a > b ? a : b);
 }
 
 cudaError_t launch_fast(int kind, const FastArgs& a, cudaStream_t s, int* grid_out) {

@@ -144,31 +144,90 @@ __global__ void k_rec_pack(const float* __restrict__ vals, const int* __restrict
 // ---------------------------------------------------------------------------
 // encoder / head / loss / optimizer
 // ---------------------------------------------------------------------------
-// X[p][r][m] = fma-chain_a X0[r][a]·We[a][p·w+m] + be[p·w+m]
-__global__ void k_encoder(const float* __restrict__ X0, int n, int d_in, const float* __restrict__ We, const float* __restrict__ be,
-                          int D, int w, int ld, float* __restrict__ X, float qs, float qi) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= static_cast<long long>(n) * D) return;
-    const int r = static_cast<int>(i / D), col = static_cast<int>(i % D);
-    const int p = col / w, m = col % w;
-    float acc = 0.f;
-    for (int t = 0; t < d_in; ++t) acc = fmaf(__ldg(X0 + static_cast<size_t>(r) * d_in + t), __ldg(We + static_cast<size_t>(t) * D + col), acc);
-    X[(static_cast<size_t>(p) * n + r) * ld + m] = dev::quant(__fadd_rn(acc, __ldg(be + col)), qs, qi);  // on the residual grid
+// The node-wise kernels move the n × D activation once (≈ 1 GB at c3): their
+// layouts are chosen for whole 16 B accesses. A "quad" is 4 consecutive
+// columns m..m+3 of one plane (ld is a multiple of 4); NQ = C·ld/4 quads per
+// row; padding columns m ≥ w are written as 0.
+constexpr int kEncRows = 64;  // k_encoder rows per CTA
+
+// X[p][r][m] = fma-chain_a X0[r][a]·We[a][p·w+m] + be[p·w+m] (oracle
+// encoder_forward: gemm_row, then + be, then the residual grid). Thread →
+// one quad (its DIN × 4 weights and 4 biases in registers) and the CTA's rows
+// ≡ its lane group (mod RL = 256 / NQ); one float4 store per row.
+template <int DIN>
+__global__ void __launch_bounds__(256) k_encoder(const float* __restrict__ X0, int n, int d_in, const float* __restrict__ We,
+                                                 const float* __restrict__ be, int D, int C, int w, int ld, float* __restrict__ X, float qs,
+                                                 float qi) {
+    const int L4 = ld >> 2, NQ = C * L4;
+    const int RL = NQ >= 256 ? 1 : 256 / NQ;
+    const int r0 = blockIdx.x * kEncRows, r1 = min(n, r0 + kEncRows);
+    for (int qb = 0; qb < NQ; qb += 256) {
+        const int q = NQ >= 256 ? qb + static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) % NQ;
+        const int g = NQ >= 256 ? 0 : static_cast<int>(threadIdx.x) / NQ;
+        if (g >= RL || q >= NQ) continue;
+        const int p = q / L4, m = 4 * (q - p * L4);
+        float wv[DIN][4], bv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool ok = m + j < w;
+#pragma unroll
+            for (int t = 0; t < DIN; ++t) wv[t][j] = (ok && t < d_in) ? __ldg(We + static_cast<size_t>(t) * D + p * w + m + j) : 0.f;
+            bv[j] = ok ? __ldg(be + p * w + m + j) : 0.f;
+        }
+#pragma unroll 2
+        for (int r = r0 + g; r < r1; r += RL) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const float* xr = X0 + static_cast<size_t>(r) * d_in;
+#pragma unroll
+            for (int t = 0; t < DIN; ++t) {
+                if (t < d_in) {
+                    const float xv = __ldg(xr + t);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = fmaf(xv, wv[t][j], acc[j]);
+                }
+            }
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = m + j < w ? dev::quant(__fadd_rn(acc[j], bv[j]), qs, qi) : 0.f;
+            *reinterpret_cast<float4*>(X + (static_cast<size_t>(p) * n + r) * ld + m) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+    }
 }
 
-// ŷ[r] = fma-chain_n X[r][n]·wh[n] + bh; masked MSE gradient and loss partials.
-__global__ void k_head_loss(const float* __restrict__ X, int n, int D, int w, int ld, const float* __restrict__ wh,
-                            const float* __restrict__ bh, const float* __restrict__ y, const uint8_t* __restrict__ mask, float cnt,
-                            float* __restrict__ yhat, float* __restrict__ gy, double* __restrict__ loss_part) {
+// ŷ[r] = fma-chain over col = p·w + m of X[p][r][m]·wh[col], + bh (oracle
+// head_forward); masked MSE gradient and per-CTA loss partials (mse_loss).
+// Thread t owns row r0 + t. The CTA stages 32-column slices of its rows
+// through shared memory with coalesced 16 B loads; the row stride of 33 makes
+// both the staging stores and the thread-per-row chain conflict-free.
+__global__ void __launch_bounds__(kThreads) k_head_loss(const float* __restrict__ X, int n, int C, int w, int ld, const float* __restrict__ wh,
+                                                        const float* __restrict__ bh, const float* __restrict__ y,
+                                                        const uint8_t* __restrict__ mask, float cnt, float* __restrict__ yhat,
+                                                        float* __restrict__ gy, double* __restrict__ loss_part) {
+    constexpr int SP = 33;
+    __shared__ float sm[kThreads * SP];
     __shared__ double red[kThreads / 32];
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = threadIdx.x, r0 = blockIdx.x * kThreads, r = r0 + t;
+    float acc = 0.f;
+    for (int p = 0; p < C; ++p) {
+        const float* Xp = X + (static_cast<size_t>(p) * n + r0) * ld;
+        for (int c0 = 0; c0 < w; c0 += 32) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int e = t + j * kThreads, rr = e >> 3, q = e & 7;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r0 + rr < n && c0 + 4 * q < ld) v = dev::ld4(Xp + static_cast<size_t>(rr) * ld + c0 + 4 * q);
+                float* s = sm + rr * SP + 4 * q;
+                s[0] = v.x; s[1] = v.y; s[2] = v.z; s[3] = v.w;
+            }
+            __syncthreads();
+            const int nm = w - c0 < 32 ? w - c0 : 32;
+            const float* wp = wh + p * w + c0;
+            for (int m = 0; m < nm; ++m) acc = fmaf(sm[t * SP + m], __ldg(wp + m), acc);
+            __syncthreads();
+        }
+    }
     double l = 0.0;
     if (r < n) {
-        float acc = 0.f;
-        for (int col = 0; col < D; ++col) {
-            const int p = col / w, m = col % w;
-            acc = fmaf(X[(static_cast<size_t>(p) * n + r) * ld + m], __ldg(wh + col), acc);
-        }
         const float yh = __fadd_rn(acc, __ldg(bh));
         yhat[r] = yh;
         if (mask[r]) {
@@ -180,60 +239,149 @@ __global__ void k_head_loss(const float* __restrict__ X, int n, int D, int w, in
         }
     }
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
+    if ((t & 31) == 0) red[t >> 5] = l;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         double s = 0.0;
         for (int i = 0; i < kThreads / 32; ++i) s += red[i];
         loss_part[blockIdx.x] = s;
     }
 }
 
-// G[p][r][m] = gy[r]·wh[p·w+m]; per-CTA partials of dwh = Σ_r X·gy and dbh = Σ_r gy.
-// part layout: [cta][D + 1]. Each CTA owns a contiguous row range.
-__global__ void k_head_bwd(const float* __restrict__ X, const float* __restrict__ gy, int n, int D, int w, int ld,
-                           const float* __restrict__ wh, float* __restrict__ G, double* __restrict__ part, int rows_per_cta) {
-    const int r0 = blockIdx.x * rows_per_cta;
-    const int r1 = min(n, r0 + rows_per_cta);
-    double* pp = part + static_cast<size_t>(blockIdx.x) * (D + 1);
-    for (int col = threadIdx.x; col < D; col += blockDim.x) {
-        const int p = col / w, m = col % w;
-        const float whc = __ldg(wh + col);
-        double s = 0.0;
-        for (int r = r0; r < r1; ++r) {
-            const size_t off = (static_cast<size_t>(p) * n + r) * ld + m;
-            const float g = __ldg(gy + r);
-            s += static_cast<double>(X[off]) * static_cast<double>(g);
-            G[off] = __fmul_rn(g, whc);
-        }
-        pp[col] = s;
-    }
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int r = r0; r < r1; ++r) s += static_cast<double>(gy[r]);
-        pp[D] = s;
+// Ordered combine of the CTA's RL row-lane partials into pp (deterministic):
+// lane group 0 stores, groups 1..RL−1 add in turn.
+__device__ __forceinline__ void combine_lanes(double* pp, int idx, double v, int g, int RL, bool act) {
+    for (int gg = 0; gg < RL; ++gg) {
+        if (act && g == gg) pp[idx] = gg == 0 ? v : pp[idx] + v;
+        __syncthreads();
     }
 }
 
-// dWe[t][col] = Σ_r X0[r][t]·G[r][col]; dbe[col] = Σ_r G[r][col]. part: [cta][d_in·D + D].
-__global__ void k_encoder_bwd(const float* __restrict__ X0, const float* __restrict__ G, int n, int d_in, int D, int w, int ld,
-                              double* __restrict__ part, int rows_per_cta) {
-    const int r0 = blockIdx.x * rows_per_cta;
-    const int r1 = min(n, r0 + rows_per_cta);
-    const int len = d_in * D + D;
-    double* pp = part + static_cast<size_t>(blockIdx.x) * len;
-    for (int col = threadIdx.x; col < D; col += blockDim.x) {
-        const int p = col / w, m = col % w;
-        double acc[16];
-        for (int t = 0; t < 16; ++t) acc[t] = 0.0;
-        double sb = 0.0;
-        for (int r = r0; r < r1; ++r) {
-            const double g = G[(static_cast<size_t>(p) * n + r) * ld + m];
-            sb += g;
-            for (int t = 0; t < d_in && t < 16; ++t) acc[t] += static_cast<double>(__ldg(X0 + static_cast<size_t>(r) * d_in + t)) * g;
+// Fixed-order double sum of gy over [r0, r1) by warp 0 → *out.
+__device__ __forceinline__ void warp_sum_rows(const float* __restrict__ v, int r0, int r1, double* out) {
+    if (threadIdx.x >= 32) return;
+    double s = 0.0;
+    for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += 32) s += static_cast<double>(__ldg(v + r));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// G[p][r][m] = gy[r]·wh[p·w+m]; per-CTA partials of dwh = Σ_r X·gy and
+// dbh = Σ_r gy over the CTA's contiguous row range (part layout [cta][D + 1]).
+// Thread → one quad and the rows ≡ its lane group (mod RL = 256 / NQ);
+// 32-row float FMA chunks flushed into double accumulators.
+__global__ void __launch_bounds__(256) k_head_bwd(const float* __restrict__ X, const float* __restrict__ gy, int n, int D, int C, int w, int ld,
+                                                  const float* __restrict__ wh, float* __restrict__ G, double* __restrict__ part,
+                                                  int rows_per_cta) {
+    const int L4 = ld >> 2, NQ = C * L4, RL = 256 / NQ;
+    const int tid = threadIdx.x, q = tid % NQ, g = tid / NQ;
+    const bool act = g < RL;
+    const int r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+    const int p = q / L4, m = 4 * (q - p * L4);
+    float whv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) whv[j] = m + j < w ? __ldg(wh + p * w + m + j) : 0.f;
+    double sd[4] = {0.0, 0.0, 0.0, 0.0};
+    if (act) {
+        const size_t pbase = static_cast<size_t>(p) * n;
+        for (int rc = r0 + g; rc < r1; rc += 32 * RL) {  // 32-row float chunks
+            float sf[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+            for (int rb = rc; rb < rc + 32 * RL && rb < r1; rb += 8 * RL) {  // eight rows of loads in flight
+                float4 x[8];
+                float gr[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int r = rb + u * RL;
+                    const bool ok = r < r1;
+                    gr[u] = ok ? __ldg(gy + r) : 0.f;
+                    x[u] = ok ? dev::ld4(X + (pbase + r) * ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int r = rb + u * RL;
+                    if (r < r1) {
+                        sf[0] = fmaf(x[u].x, gr[u], sf[0]); sf[1] = fmaf(x[u].y, gr[u], sf[1]);
+                        sf[2] = fmaf(x[u].z, gr[u], sf[2]); sf[3] = fmaf(x[u].w, gr[u], sf[3]);
+                        *reinterpret_cast<float4*>(G + (pbase + r) * ld + m) =
+                            make_float4(m < w ? __fmul_rn(gr[u], whv[0]) : 0.f, m + 1 < w ? __fmul_rn(gr[u], whv[1]) : 0.f,
+                                        m + 2 < w ? __fmul_rn(gr[u], whv[2]) : 0.f, m + 3 < w ? __fmul_rn(gr[u], whv[3]) : 0.f);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sd[j] += static_cast<double>(sf[j]);
         }
-        for (int t = 0; t < d_in && t < 16; ++t) pp[t * D + col] = acc[t];
-        pp[d_in * D + col] = sb;
+    }
+    double* pp = part + static_cast<size_t>(blockIdx.x) * (D + 1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) combine_lanes(pp, p * w + (m + j < w ? m + j : 0), sd[j], g, RL, act && m + j < w);
+    warp_sum_rows(gy, r0, r1, pp + D);
+}
+
+// dWe[t][col] = Σ_r X0[r][t]·G[r][col]; dbe[col] = Σ_r G[r][col]
+// (part layout [cta][d_in·D + D]); the k_head_bwd thread layout, DIN ≥ d_in.
+template <int DIN>
+__global__ void __launch_bounds__(256, 2) k_encoder_bwd(const float* __restrict__ X0, const float* __restrict__ G, int n, int d_in, int D, int C,
+                                                     int w, int ld, double* __restrict__ part, int rows_per_cta) {
+    const int L4 = ld >> 2, NQ = C * L4, RL = 256 / NQ;
+    const int tid = threadIdx.x, q = tid % NQ, g = tid / NQ;
+    const bool act = g < RL;
+    const int r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+    const int p = q / L4, m = 4 * (q - p * L4);
+    double sd[DIN + 1][4];
+#pragma unroll
+    for (int t = 0; t <= DIN; ++t)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sd[t][j] = 0.0;
+    if (act) {
+        const size_t pbase = static_cast<size_t>(p) * n;
+        for (int rc = r0 + g; rc < r1; rc += 32 * RL) {
+            float sf[DIN + 1][4];
+#pragma unroll
+            for (int t = 0; t <= DIN; ++t)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) sf[t][j] = 0.f;
+#pragma unroll 1
+            for (int rb = rc; rb < rc + 32 * RL && rb < r1; rb += 4 * RL) {  // four rows of loads in flight
+                float4 gv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int r = rb + u * RL;
+                    gv[u] = r < r1 ? dev::ld4(G + (pbase + r) * ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int r = rb + u * RL;
+                    if (r < r1) {
+                        const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+                        const float* xr = X0 + static_cast<size_t>(r) * d_in;
+#pragma unroll
+                        for (int t = 0; t < DIN; ++t) {
+                            const float xv = t < d_in ? __ldg(xr + t) : 0.f;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) sf[t][j] = fmaf(xv, gg[j], sf[t][j]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) sf[DIN][j] = __fadd_rn(sf[DIN][j], gg[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t <= DIN; ++t)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) sd[t][j] += static_cast<double>(sf[t][j]);
+        }
+    }
+    double* pp = part + static_cast<size_t>(blockIdx.x) * (d_in * D + D);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool ok = act && m + j < w;
+        const int col = p * w + (m + j < w ? m + j : 0);
+#pragma unroll
+        for (int t = 0; t < DIN; ++t)
+            if (t < d_in) combine_lanes(pp, t * D + col, sd[t][j], g, RL, ok);
+        combine_lanes(pp, d_in * D + col, sd[DIN][j], g, RL, ok);
     }
 }
 
@@ -407,35 +555,35 @@ cudaError_t launch_rec_pack(const float* vals, const int* idx, int n, int k, uin
 
 cudaError_t launch_encoder(const float* X0, int n, int d_in, const float* We, const float* be, int D, int C, int w, int ld, float* X,
                            float qs, float qi, cudaStream_t s) {
-    (void)C;
-    const long long tot = static_cast<long long>(n) * D;
-    if (!tot) return cudaSuccess;
-    k_encoder<<<blocks_for(tot, 256), 256, 0, s>>>(X0, n, d_in, We, be, D, w, ld, X, qs, qi);
+    if (!n) return cudaSuccess;
+    if (d_in > 16) return cudaErrorInvalidValue;
+    if (d_in <= 8) k_encoder<8><<<blocks_for(n, kEncRows), 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
+    else k_encoder<16><<<blocks_for(n, kEncRows), 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
     return cudaGetLastError();
 }
 
 cudaError_t launch_head_loss(const float* X, int n, int D, int C, int w, int ld, const float* wh, const float* bh, const float* y,
                              const uint8_t* mask, float, float cnt, float* yhat, float* gy, double* loss_part, int nparts, cudaStream_t s) {
-    (void)C;
+    (void)D;
     (void)nparts;
-    k_head_loss<<<blocks_for(n, kThreads), kThreads, 0, s>>>(X, n, D, w, ld, wh, bh, y, mask, cnt, yhat, gy, loss_part);
+    k_head_loss<<<blocks_for(n, kThreads), kThreads, 0, s>>>(X, n, C, w, ld, wh, bh, y, mask, cnt, yhat, gy, loss_part);
     return cudaGetLastError();
 }
 
 cudaError_t launch_head_bwd(const float* X, const float* gy, int n, int D, int C, int w, int ld, const float* wh, float* G, double* part,
                             int nparts, cudaStream_t s) {
-    (void)C;
+    if (C * (ld / 4) > 256) return cudaErrorInvalidValue;
     const int rows = (n + nparts - 1) / nparts;
-    k_head_bwd<<<nparts, 256, 0, s>>>(X, gy, n, D, w, ld, wh, G, part, rows);
+    k_head_bwd<<<nparts, 256, 0, s>>>(X, gy, n, D, C, w, ld, wh, G, part, rows);
     return cudaGetLastError();
 }
 
 cudaError_t launch_encoder_bwd(const float* X0, const float* G, int n, int d_in, int D, int C, int w, int ld, double* part, int nparts,
                                cudaStream_t s) {
-    (void)C;
-    if (d_in > 16) return cudaErrorInvalidValue;
+    if (d_in > 16 || C * (ld / 4) > 256) return cudaErrorInvalidValue;
     const int rows = (n + nparts - 1) / nparts;
-    k_encoder_bwd<<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, w, ld, part, rows);
+    if (d_in <= 8) k_encoder_bwd<8><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    else k_encoder_bwd<16><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
     return cudaGetLastError();
 }
 

@@ -125,6 +125,7 @@ struct FastArgs {
 };
 
 bool fast_supported(int w, int k);
+int fast_bin_grid_max();  // largest BIN grid (dW partial slots) of the fast path
 // TMA map of an n × ld fp32 plane in 128-row × 32-column boxes, SWIZZLE_128B
 // (the boxes land in exactly the UMMA K-major SW128 tile layout of fast.cu).
 cudaError_t encode_plane_map(CUtensorMap* m, const float* base, int n, int ld);
