@@ -347,8 +347,9 @@ __device__ __forceinline__ uint32_t gs_key(float v, int col, int w) {
     return col < w ? (__float_as_uint(v) & 0x7fffffffu) + 1u : 0u;
 }
 
-template <int W, bool FULLW>
-__device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
+template <int W, bool FULLW, int K = 0>
+__device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k_rt, uint8_t* rec_out) {
+    const int k = K ? K : k_rt;  // K: k at compile time (0: any k ≤ 16)
     constexpr int G = 16;
     constexpr int LW = W == 64 ? 6 : 5;
     static_assert((1 << LW) == W, "W must be 32 or 64");
@@ -447,15 +448,20 @@ __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k
     uint32_t iw[4] = {0u, 0u, 0u, 0u};
     float rv[16];
     uint32_t m0 = ge[0], m1 = NWD > 1 ? ge[NWD - 1] : 0u;
+    const float* trow = Ts + r * 32;
+    const int rx = (r & 7) << 2;
 #pragma unroll
     for (int slot = 0; slot < 16; ++slot) {
         rv[slot] = 0.f;
-        if (slot < k) {
-            int col;
-            if (m0) { col = __ffs(m0) - 1; m0 &= m0 - 1u; }
-            else { col = 32 + __ffs(m1) - 1; m1 &= m1 - 1u; }
+        if (slot < k) {  // branch-free: the lowest set bit of m0, else of m1
+            const bool lo = m0 != 0u;
+            const uint32_t mm = lo ? m0 : m1;
+            const int col = __ffs(mm) - 1 + (lo ? 0 : 32);
+            const uint32_t cl = mm & (mm - 1u);
+            m0 = lo ? cl : m0;
+            m1 = lo ? m1 : cl;
             iw[slot >> 2] |= static_cast<uint32_t>(col) << (8 * (slot & 3));
-            rv[slot] = Ts[zo(r, col)];
+            rv[slot] = trow[(col >> 5) * (TR * 32) + ((col ^ rx) & 31)];  // Ts[zo(r, col)]
         }
     }
     uint4* o = reinterpret_cast<uint4*>(rec_out);
@@ -466,10 +472,11 @@ __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k
         if (q < nv4) reinterpret_cast<float4*>(rec_out + 16)[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
 }
 
-template <int W, int G>
+template <int W, int G, int K = 0>
 __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
     static_assert(G == 16, "top-16 tree (k ≤ 16)");
-    if (w == W) gs_row_impl<W, true>(Ts, r, w, k, rec_out);
+    if (K && k == K && w == W) gs_row_impl<W, true, K>(Ts, r, w, k, rec_out);
+    else if (w == W) gs_row_impl<W, true>(Ts, r, w, k, rec_out);
     else gs_row_impl<W, false>(Ts, r, w, k, rec_out);
 }
 
@@ -723,26 +730,32 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
             bulk_load(Win + (jj & 1) * (Pl::win * 4), a.rec_in + static_cast<size_t>(lo) * RB, static_cast<uint32_t>(cnt * RB), wb);
         };
         if (t == 0 && my_tiles > 0) issue_win(0);
+        // this row's neighbour slots and row scale, loaded one tile ahead
+        int cv[kSegF];
+        float sv[kSegF];
+        int ne = 0;
+        float rf = 0.f;
+        auto load_meta = [&](int jj) {
+            const int rw = tile_of(jj) * TR + t;
+            ne = 0;
+            rf = 0.f;
+            if (jj < my_tiles && rw < a.n) {
+                ne = load_ell_row(a.dir.ell, rw, cv, sv);
+                rf = __ldg(a.dir.out_f + rw);
+            }
+        };
+        load_meta(0);
         for (int j = 0; j < my_tiles; ++j) {
             const int tile_i = tile_of(j);
             const int row0 = tile_i * TR, row = row0 + t;
-            const bool valid = row < a.n;
             const int b = j & 1;
             if (KIND == INV && j == my_tiles - 1) dev::pdl_trigger();
             if (t == 0) {
-                prefetch_tile_meta(a.dir, tile_i + static_cast<int>(gridDim.x), n_tiles, a.n);
+                prefetch_tile_meta(a.dir, tile_i + 2 * static_cast<int>(gridDim.x), n_tiles, a.n);
                 if (j + 1 < my_tiles) {  // Win[(j + 1) & 1] was last read by tile j − 1 (before its barriers)
                     tile::fence_proxy_async();
                     issue_win(j + 1);
                 }
-            }
-            float rf = 0.f;
-            int ne = 0;
-            int cv[kSegF];
-            float sv[kSegF];
-            if (valid) {
-                ne = load_ell_row(a.dir.ell, row, cv, sv);
-                rf = __ldg(a.dir.out_f + row);
             }
             RecWin wn;
             win_span(j, wn.lo, wn.cnt);
@@ -787,6 +800,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
                          desc_sw128(wa + (kk >> 2) * (W * 128) + (kk & 3) * 32, 16), idesc<W>(0, 0), kk > 0 ? 1u : 0u);
                 tile::umma_commit(&bar[b]);
             }
+            load_meta(j + 1);
         }
     } else {
         // ================= epilogue group (warps 4-7) =================
@@ -838,7 +852,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
                 for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Ob + (c >> 5) * (TR * 32), c, row0);
                 tma_store_commit();
             }
-            if (a.gs_out && valid) gs_row<W, 16>(Ob, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+            if (a.gs_out && valid) gs_row<W, 16, KS == 16 ? 16 : 0>(Ob, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
             named_bar_sync(2, TR);  // every read of Out is done
             if (t == 0) {
                 tma_store_wait_read();
