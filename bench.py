@@ -162,11 +162,14 @@ class ClockSampler:
 
 def load_traffic(cfg_name):
     """Measured DRAM bytes per launch (ncu --set full, committed under profiles/) for the c3 kernel classes."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if cfg_name != "c3" or not os.path.exists(p):
+    if cfg_name != "c3":
         return {}
-    with open(p) as f:
-        return json.load(f)
+    for name in ("r2_traffic.json", "r1_traffic.json"):  # the latest round's capture
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            with open(p) as f:
+                return json.load(f)
+    return {}
 
 
 def build_inputs(cfg_name, rank):

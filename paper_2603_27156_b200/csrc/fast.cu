@@ -15,7 +15,12 @@
 //        inverse pass never reads G_i (db_i = colsum G_i: k_colsum, bias only)
 //
 // Design (persistent CTAs, one 128-row tile at a time):
-//   * FWD / INV (128 threads): thread t owns tile row t end to end. It reads its
+//   * FWD / INV run as k_fws (below): the CTA's aggregation warps build tile
+//     j's A operand from a shared-memory window of the neighbour records while
+//     its epilogue warps finish tile j − 1 (residual, TMA store, GS top-k), with
+//     two TMEM accumulators. k_fast is the single-group form of the same
+//     arithmetic (the rev-baseline's dense FWD / INV, and the A/B switch
+//     GSRC_NO_WS). In k_fast thread t owns tile row t end to end. It reads its
 //     row's 8 neighbour slots (Dir::ell, row-addressed), walks its ≤ kSeg
 //     edges (longer "hub" rows come pre-aggregated from k_hub_rows in the
 //     oracle's canonical segment order), accumulates in its column of a
@@ -39,7 +44,7 @@
 // Arithmetic per row is the oracle's (oracle/gsr_oracle.hpp, TF32 mode):
 // canonical segmented aggregation, row scale; fp32 operands are handed to the
 // tensor core as they are, which reads them as TF32 by truncating the low 13
-// mantissa bits (measured on the device, scratch/tf32_probe.cu) — the oracle
+// mantissa bits (tests/test_gpu_config_parity.py test_fast_path_tf32_operand_truncation) — the oracle
 // truncates the same operands.
 #include "tile.cuh"
 

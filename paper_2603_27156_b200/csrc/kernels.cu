@@ -174,16 +174,26 @@ __global__ void __launch_bounds__(256) k_encoder(const float* __restrict__ X0, i
             for (int t = 0; t < DIN; ++t) wv[t][j] = (ok && t < d_in) ? __ldg(We + static_cast<size_t>(t) * D + p * w + m + j) : 0.f;
             bv[j] = ok ? __ldg(be + p * w + m + j) : 0.f;
         }
-#pragma unroll 2
+#pragma unroll 4
         for (int r = r0 + g; r < r1; r += RL) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             const float* xr = X0 + static_cast<size_t>(r) * d_in;
+            float xv[DIN];
+            if (d_in == DIN) {  // whole 16 B loads of the input row
+#pragma unroll
+                for (int t = 0; t < DIN; t += 4) {
+                    const float4 v = dev::ld4(xr + t);
+                    xv[t] = v.x; xv[t + 1] = v.y; xv[t + 2] = v.z; xv[t + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < DIN; ++t) xv[t] = t < d_in ? __ldg(xr + t) : 0.f;
+            }
 #pragma unroll
             for (int t = 0; t < DIN; ++t) {
                 if (t < d_in) {
-                    const float xv = __ldg(xr + t);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[j] = fmaf(xv, wv[t][j], acc[j]);
+                    for (int j = 0; j < 4; ++j) acc[j] = fmaf(xv[t], wv[t][j], acc[j]);
                 }
             }
             float o[4];
@@ -320,62 +330,88 @@ __global__ void __launch_bounds__(256) k_head_bwd(const float* __restrict__ X, c
 }
 
 // dWe[t][col] = Σ_r X0[r][t]·G[r][col]; dbe[col] = Σ_r G[r][col]
-// (part layout [cta][d_in·D + D]); the k_head_bwd thread layout, DIN ≥ d_in.
-template <int DIN>
+// (part layout [cta][d_in·D + D]). Thread → V consecutive columns of a plane
+// (NV = C·ld/V per row) and the CTA's rows ≡ its lane group (mod RL = 256/NV);
+// 32-row float FMA chunks flushed into double accumulators (V = 2 keeps the
+// (DIN + 1)·V doubles in registers); lane groups combined in fixed order.
+template <int DIN, int V>
 __global__ void __launch_bounds__(256, 2) k_encoder_bwd(const float* __restrict__ X0, const float* __restrict__ G, int n, int d_in, int D, int C,
-                                                     int w, int ld, double* __restrict__ part, int rows_per_cta) {
-    const int L4 = ld >> 2, NQ = C * L4, RL = 256 / NQ;
-    const int tid = threadIdx.x, q = tid % NQ, g = tid / NQ;
+                                                        int w, int ld, double* __restrict__ part, int rows_per_cta) {
+    const int LV = ld / V, NV = C * LV, RL = 256 / NV;
+    const int tid = threadIdx.x, q = tid % NV, g = tid / NV;
     const bool act = g < RL;
     const int r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
-    const int p = q / L4, m = 4 * (q - p * L4);
-    double sd[DIN + 1][4];
+    const int p = q / LV, m = V * (q - p * LV);
+    double sd[DIN + 1][V];
 #pragma unroll
     for (int t = 0; t <= DIN; ++t)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sd[t][j] = 0.0;
+        for (int j = 0; j < V; ++j) sd[t][j] = 0.0;
+    auto ldv = [&](const float* ptr, float (&o)[V]) {
+        if constexpr (V == 4) {
+            const float4 v = dev::ld4(ptr);
+            o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+        } else {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(ptr));
+            o[0] = v.x; o[1] = v.y;
+        }
+    };
     if (act) {
         const size_t pbase = static_cast<size_t>(p) * n;
         for (int rc = r0 + g; rc < r1; rc += 32 * RL) {
-            float sf[DIN + 1][4];
+            float sf[DIN + 1][V];
 #pragma unroll
             for (int t = 0; t <= DIN; ++t)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) sf[t][j] = 0.f;
+                for (int j = 0; j < V; ++j) sf[t][j] = 0.f;
 #pragma unroll 1
             for (int rb = rc; rb < rc + 32 * RL && rb < r1; rb += 4 * RL) {  // four rows of loads in flight
-                float4 gv[4];
+                float gv[4][V];
+                float xv[4][DIN];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int r = rb + u * RL;
-                    gv[u] = r < r1 ? dev::ld4(G + (pbase + r) * ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const bool ok = r < r1;
+#pragma unroll
+                    for (int j = 0; j < V; ++j) gv[u][j] = 0.f;
+#pragma unroll
+                    for (int t = 0; t < DIN; ++t) xv[u][t] = 0.f;
+                    if (ok) {
+                        ldv(G + (pbase + r) * ld + m, gv[u]);
+                        const float* xr = X0 + static_cast<size_t>(r) * d_in;
+                        if (d_in == DIN) {
+#pragma unroll
+                            for (int t = 0; t < DIN; t += 4) {
+                                const float4 v = dev::ld4(xr + t);
+                                xv[u][t] = v.x; xv[u][t + 1] = v.y; xv[u][t + 2] = v.z; xv[u][t + 3] = v.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < DIN; ++t) xv[u][t] = t < d_in ? __ldg(xr + t) : 0.f;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int r = rb + u * RL;
-                    if (r < r1) {
-                        const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
-                        const float* xr = X0 + static_cast<size_t>(r) * d_in;
+                    if (rb + u * RL < r1) {
 #pragma unroll
-                        for (int t = 0; t < DIN; ++t) {
-                            const float xv = t < d_in ? __ldg(xr + t) : 0.f;
+                        for (int t = 0; t < DIN; ++t)
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) sf[t][j] = fmaf(xv, gg[j], sf[t][j]);
-                        }
+                            for (int j = 0; j < V; ++j) sf[t][j] = fmaf(xv[u][t], gv[u][j], sf[t][j]);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) sf[DIN][j] = __fadd_rn(sf[DIN][j], gg[j]);
+                        for (int j = 0; j < V; ++j) sf[DIN][j] = __fadd_rn(sf[DIN][j], gv[u][j]);
                     }
                 }
             }
 #pragma unroll
             for (int t = 0; t <= DIN; ++t)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) sd[t][j] += static_cast<double>(sf[t][j]);
+                for (int j = 0; j < V; ++j) sd[t][j] += static_cast<double>(sf[t][j]);
         }
     }
     double* pp = part + static_cast<size_t>(blockIdx.x) * (d_in * D + D);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < V; ++j) {
         const bool ok = act && m + j < w;
         const int col = p * w + (m + j < w ? m + j : 0);
 #pragma unroll
@@ -582,8 +618,14 @@ cudaError_t launch_encoder_bwd(const float* X0, const float* G, int n, int d_in,
                                cudaStream_t s) {
     if (d_in > 16 || C * (ld / 4) > 256) return cudaErrorInvalidValue;
     const int rows = (n + nparts - 1) / nparts;
-    if (d_in <= 8) k_encoder_bwd<8><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
-    else k_encoder_bwd<16><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    const bool pairs = C * (ld / 2) <= 256;  // two columns per thread when a row's pairs fit one CTA
+    if (d_in <= 8) {
+        if (pairs) k_encoder_bwd<8, 2><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+        else k_encoder_bwd<8, 4><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    } else {
+        if (pairs) k_encoder_bwd<16, 2><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+        else k_encoder_bwd<16, 4><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    }
     return cudaGetLastError();
 }
 

@@ -203,7 +203,7 @@ struct AggMeta {
 };
 
 // An fp32 value as the UMMA kind::tf32 path reads it: low 13 mantissa bits
-// truncated (measured on the B200, scratch/tf32_probe.cu; oracle tf32_op).
+// truncated (tests/test_gpu_config_parity.py test_fast_path_tf32_operand_truncation; oracle tf32_op).
 // Used where the CUDA cores must reproduce a tensor-core operand.
 __device__ __forceinline__ float tf32_op(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 

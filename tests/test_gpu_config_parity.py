@@ -1,5 +1,5 @@
 """GPU ↔ oracle parity at the BASELINE.json configs, and a bit-exact test of the
-benched TF32 fast-path kernels (k_fast FWD / INV, k_bin2, k_gs_tma, k_hub_*).
+benched TF32 fast-path kernels (k_fws FWD / INV, k_bin2, k_gs_tma, k_hub_*).
 
 * c1 exactly (N=10k, E≈40k, L=8, D=64, C=2, k=8), ALG12 and GSR-C, FP32-strict:
   predictions and activations bit-exact, loss and gradients within 1e-4.
@@ -263,3 +263,38 @@ def test_fast_path_dyadic_bit_exact(ctx, oracle_tf32, D, C, k, bias):
     dg, rgr = ctx.grads(), net.grads()
     assert np.abs(rgr).max() > 0
     assert np.array_equal(dg, rgr), np.abs(dg - rgr).max()
+
+
+# ---- (v) TF32 operand truncation, on the benched FWD / INV kernels ------------------------
+@pytest.mark.parametrize("D,C,k", [(256, 4, 16), (128, 4, 8)])
+def test_fast_path_tf32_operand_truncation(ctx, oracle_tf32, D, C, k):
+    """The tensor core reads an fp32 operand as TF32 by truncating its low 13
+    mantissa bits; the oracle's TF32 mode (tf32_op) assumes exactly that. With
+    the dyadic case's signed-permutation transforms but full-mantissa
+    activations, every MMA output of blocks 0 and C-1 is one product
+    ±trunc(z) of a full-mantissa aggregate z, so FWD and INV must match the
+    oracle bit for bit; rounding instead of truncating would change about half
+    of those outputs by one TF32 ulp (≫ the 2^-20 residual grid)."""
+    from paper_2603_27156_b200 import GEMM_TF32, MODE_GSRC, NORM_NONE
+    oracle = oracle_tf32
+    n = 4000
+    g, p, _, _, _ = dyadic_case(n, D, C, k, seed=7 + D + k, use_bias=False)
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(n, D)).astype(np.float32)
+    assert ((x.view(np.uint32) & 0x1FFF) != 0).mean() > 0.99  # low mantissa bits present
+    ctx.graph_upload(g.row_ptr, g.col_idx, norm=NORM_NONE)
+    og = oracle.Graph(g.row_ptr, g.col_idx, norm=NORM_NONE)
+    ctx.model_init(MODE_GSRC, 1, D, C, k, 8, use_bias=False, gemm=GEMM_TF32)
+    net = oracle.Net(og, MODE_GSRC, 1, D, C, k, 8, use_bias=False, dtype=np.float32)
+    ctx.set_params(p)
+    net.set_params(p)
+    ctx.set_activation(x)
+    ctx.layer_forward(0)
+    y = ctx.activation()
+    ry = net.layer_forward(0, x)
+    w = D // C
+    changed = np.abs(ry[:, :w] - x[:, :w]) > 0   # block 0 moved these values: ±trunc(z) landed there
+    assert changed.mean() > 0.5
+    assert np.array_equal(y, ry), np.abs(y - ry).max()
+    ctx.layer_inverse(0)
+    assert np.array_equal(ctx.activation(), net.layer_inverse(0, ry))

@@ -1,6 +1,6 @@
 """Thread-per-row tcgen05 fast path (csrc/fast.cu) ↔ oracle in TF32 mode.
 
-The GSR-C step in TF32 mode runs k_fast FWD / INV / BIN plus the k_hub
+The GSR-C step in TF32 mode runs k_fws FWD / INV, k_bin2 BIN plus the k_hub
 pre-pass for rows longer than one aggregation segment. The oracle in TF32 mode
 (oracle.set_tf32) truncates the same operands to TF32 that the tensor core does, so the
 two differ only by the tensor core's accumulation order; bounds as stated in
