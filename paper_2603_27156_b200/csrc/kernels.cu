@@ -154,10 +154,11 @@ constexpr int kEncRows = 64;  // k_encoder rows per CTA
 // encoder_forward: gemm_row, then + be, then the residual grid). Thread →
 // one quad (its DIN × 4 weights and 4 biases in registers) and the CTA's rows
 // ≡ its lane group (mod RL = 256 / NQ); one float4 store per row.
-template <int DIN>
-__global__ void __launch_bounds__(256) k_encoder(const float* __restrict__ X0, int n, int d_in, const float* __restrict__ We,
+template <int DIN, bool EXACT>
+__global__ void __launch_bounds__(256) k_encoder(const float* __restrict__ X0, int n, int d_in_rt, const float* __restrict__ We,
                                                  const float* __restrict__ be, int D, int C, int w, int ld, float* __restrict__ X, float qs,
                                                  float qi) {
+    const int d_in = EXACT ? DIN : d_in_rt;  // EXACT: d_in is DIN, every input-width check folds away
     const int L4 = ld >> 2, NQ = C * L4;
     const int RL = NQ >= 256 ? 1 : 256 / NQ;
     const int r0 = blockIdx.x * kEncRows, r1 = min(n, r0 + kEncRows);
@@ -334,9 +335,10 @@ __global__ void __launch_bounds__(256) k_head_bwd(const float* __restrict__ X, c
 // (NV = C·ld/V per row) and the CTA's rows ≡ its lane group (mod RL = 256/NV);
 // 32-row float FMA chunks flushed into double accumulators (V = 2 keeps the
 // (DIN + 1)·V doubles in registers); lane groups combined in fixed order.
-template <int DIN, int V>
-__global__ void __launch_bounds__(256, 2) k_encoder_bwd(const float* __restrict__ X0, const float* __restrict__ G, int n, int d_in, int D, int C,
+template <int DIN, int V, bool EXACT>
+__global__ void __launch_bounds__(256, 2) k_encoder_bwd(const float* __restrict__ X0, const float* __restrict__ G, int n, int d_in_rt, int D, int C,
                                                         int w, int ld, double* __restrict__ part, int rows_per_cta) {
+    const int d_in = EXACT ? DIN : d_in_rt;  // EXACT: d_in is DIN, every input-width check folds away
     const int LV = ld / V, NV = C * LV, RL = 256 / NV;
     const int tid = threadIdx.x, q = tid % NV, g = tid / NV;
     const bool act = g < RL;
@@ -593,8 +595,10 @@ cudaError_t launch_encoder(const float* X0, int n, int d_in, const float* We, co
                            float qs, float qi, cudaStream_t s) {
     if (!n) return cudaSuccess;
     if (d_in > 16) return cudaErrorInvalidValue;
-    if (d_in <= 8) k_encoder<8><<<blocks_for(n, kEncRows), 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
-    else k_encoder<16><<<blocks_for(n, kEncRows), 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
+    const int g = blocks_for(n, kEncRows);
+    if (d_in == 8) k_encoder<8, true><<<g, 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
+    else if (d_in < 8) k_encoder<8, false><<<g, 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
+    else k_encoder<16, false><<<g, 256, 0, s>>>(X0, n, d_in, We, be, D, C, w, ld, X, qs, qi);
     return cudaGetLastError();
 }
 
@@ -619,12 +623,13 @@ cudaError_t launch_encoder_bwd(const float* X0, const float* G, int n, int d_in,
     if (d_in > 16 || C * (ld / 4) > 256) return cudaErrorInvalidValue;
     const int rows = (n + nparts - 1) / nparts;
     const bool pairs = C * (ld / 2) <= 256;  // two columns per thread when a row's pairs fit one CTA
-    if (d_in <= 8) {
-        if (pairs) k_encoder_bwd<8, 2><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
-        else k_encoder_bwd<8, 4><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    if (d_in == 8 && pairs) k_encoder_bwd<8, 2, true><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+    else if (d_in <= 8) {
+        if (pairs) k_encoder_bwd<8, 2, false><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+        else k_encoder_bwd<8, 4, false><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
     } else {
-        if (pairs) k_encoder_bwd<16, 2><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
-        else k_encoder_bwd<16, 4><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+        if (pairs) k_encoder_bwd<16, 2, false><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
+        else k_encoder_bwd<16, 4, false><<<nparts, 256, 0, s>>>(X0, G, n, d_in, D, C, w, ld, part, rows);
     }
     return cudaGetLastError();
 }
