@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../gsr_cuda.h"
@@ -178,6 +179,13 @@ public:
         check(gsrc_kernel_launches(h_, &n), h_, "kernel_launches");
         return n;
     }
+    // WorkCounter: {scalar_mul_adds, rows_touched} since create / work_reset()
+    std::pair<std::uint64_t, std::uint64_t> work_counter() const {
+        std::uint64_t ma = 0, rows = 0;
+        check(gsrc_work_counter(h_, &ma, &rows), h_, "work_counter");
+        return {ma, rows};
+    }
+    void work_reset() { check(gsrc_work_reset(h_), h_, "work_reset"); }
 
 private:
     gsrc_ctx* h_ = nullptr;

@@ -114,6 +114,16 @@ int gsrc_last_timing(gsrc_ctx* ctx, gsrc_timing* out);
 int gsrc_mem_stats(gsrc_ctx* ctx, gsrc_mem_report* out);                  /* Arena::stats SPEC.md:486-490 */
 int gsrc_high_water_reset(gsrc_ctx* ctx);
 int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out);                    /* kernels enqueued since create */
+/* WorkCounter: scalar multiply-adds and rows touched of the
+   SPEC operations executed since create / the last reset, with the oracle's
+   accounting — gsr_forward_block e·k + n·w² with W (also each
+   block of gsrc_layer_forward / gsrc_layer_inverse and of the steps),
+   gsr_backward_block e·k + n·w² + e·w with W (Alg. 2 layers), spmm e·cols and
+   spmm_sparse e·k (+ n rows). Counted per call, so CUDA graph
+   replays count; the rev-baseline's dense blocks and the grouped-reversible
+   exact-chain-rule backward have no SPEC work formula and add 0. */
+int gsrc_work_counter(gsrc_ctx* ctx, uint64_t* scalar_mul_adds, uint64_t* rows_touched);
+int gsrc_work_reset(gsrc_ctx* ctx);
 /* Live per-kernel timing for the roofline report. out must hold 16 + 3·C
    doubles: out[0..15] = 4 kernel classes × {ms per launch (mean over the C
    blocks), algorithmic bytes per launch, launches per step, flops per launch},

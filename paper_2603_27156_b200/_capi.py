@@ -68,7 +68,7 @@ EXPORTS = [
     "gsrc_zero_grads", "gsrc_grads_device", "gsrc_params_device", "gsrc_data_upload", "gsrc_forward", "gsrc_forward_backward",
     "gsrc_optimizer_step", "gsrc_train_step", "gsrc_activation_get", "gsrc_activation_set", "gsrc_gradient_get",
     "gsrc_gradient_set", "gsrc_set_graph_capture", "gsrc_last_timing", "gsrc_mem_stats", "gsrc_high_water_reset",
-    "gsrc_kernel_launches", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
+    "gsrc_kernel_launches", "gsrc_work_counter", "gsrc_work_reset", "gsrc_profile_kernels", "gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward", "gsrc_op_gs_topk",
     "gsrc_set_op_precision", "gsrc_op_spmm", "gsrc_op_spmm_sparse", "gsrc_op_block_forward", "gsrc_op_dense_block", "gsrc_op_block_backward",
     "gsrc_get_stream", "gsrc_optim_state_get", "gsrc_optim_state_set", "gsrc_comm_unique_id", "gsrc_comm_init",
     "gsrc_comm_allreduce_grads", "gsrc_comm_destroy", "gsrc_diag_masks", "gsrc_diag_mask_flips", "gsrc_set_residual_quant",
@@ -110,6 +110,8 @@ def lib():
         L.gsrc_last_timing.argtypes = [vp, C.POINTER(Timing)]
         L.gsrc_mem_stats.argtypes = [vp, C.POINTER(MemReport)]
         L.gsrc_kernel_launches.argtypes = [vp, C.POINTER(i64)]
+        L.gsrc_work_counter.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.gsrc_work_reset.argtypes = [vp]
         L.gsrc_profile_kernels.argtypes = [vp, i32, vp]
         for nm in ("gsrc_layer_forward", "gsrc_layer_inverse", "gsrc_layer_backward"):
             getattr(L, nm).argtypes = [vp, i32]
@@ -317,6 +319,15 @@ class Context:
 
     def high_water_reset(self):
         self._chk(lib().gsrc_high_water_reset(self.h))
+
+    def work_counter(self):
+        """WorkCounter: (scalar_mul_adds, rows_touched) since create / work_reset()."""
+        ma, rows = C.c_uint64(), C.c_uint64()
+        self._chk(lib().gsrc_work_counter(self.h, C.byref(ma), C.byref(rows)))
+        return ma.value, rows.value
+
+    def work_reset(self):
+        self._chk(lib().gsrc_work_reset(self.h))
 
     def kernel_launches(self):
         n = C.c_int64()

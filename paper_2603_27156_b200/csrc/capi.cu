@@ -155,6 +155,15 @@ struct gsrc_ctx {
     cudaStream_t own = nullptr;
     std::string err;
     int64_t launches = 0;
+    // WorkCounter: the scalar multiply-adds and rows touched of
+    // the SPEC operations executed, counted per call of an entry point (CUDA
+    // graph replays included), with the oracle's accounting (oracle/
+    // gsr_oracle.hpp): gsr_forward_block e·k + n·w² with W,
+    // gsr_backward_block e·k + (n·w² + e·w with W), spmm e·cols and
+    // spmm_sparse e·k (+ n rows each). The rev-baseline's
+    // dense blocks and the exact-chain-rule backward of the grouped-reversible
+    // modes are composite operations without a SPEC work formula: not counted.
+    uint64_t work_ma = 0, work_rows = 0;
 
     // persistent: graph
     int64_t n = 0, e = 0;
@@ -737,6 +746,22 @@ struct gsrc_ctx {
         filled[l] = 0;
     }
 
+    // ---- WorkCounter formulas (per layer, this model) ------------------------------
+    uint64_t work_block_fwd(int w_, int k_, bool uw) const {
+        return static_cast<uint64_t>(e) * k_ + (uw ? static_cast<uint64_t>(n) * w_ * w_ : 0);
+    }
+    uint64_t work_block_bwd(int w_, int k_, bool uw) const {
+        return static_cast<uint64_t>(e) * k_ + (uw ? static_cast<uint64_t>(n) * w_ * w_ + static_cast<uint64_t>(e) * w_ : 0);
+    }
+    uint64_t work_layer_fwd() const {
+        if (cfg.mode == GSRC_MODE_REV) return 0;
+        return static_cast<uint64_t>(cfg.mode == GSRC_MODE_ALG12 ? 2 : C) * work_block_fwd(w, k, cfg.use_weight != 0);
+    }
+    uint64_t work_layer_bwd() const {  // Alg. 2: two recomputed forward blocks (lines 5-7) and two backward blocks
+        if (cfg.mode != GSRC_MODE_ALG12) return 0;
+        return 2 * work_block_fwd(w, k, cfg.use_weight != 0) + 2 * work_block_bwd(w, k, cfg.use_weight != 0);
+    }
+
     // ---- network ---------------------------------------------------------------
     void layer_forward(int l) { if (cfg.mode == GSRC_MODE_ALG12) alg12_layer_forward(l); else rev_layer_forward(l); }
     void layer_backward(int l) { if (cfg.mode == GSRC_MODE_ALG12) alg12_layer_backward(l); else rev_layer_backward(l); }
@@ -1258,6 +1283,7 @@ int gsrc_forward(gsrc_ctx* ctx, float* yhat_out) {
     return guarded(ctx, [&] {
         ctx->require_data();
         ctx->enqueue_forward();
+        ctx->work_ma += static_cast<uint64_t>(ctx->cfg.layers) * ctx->work_layer_fwd();
         if (yhat_out) CK(cudaMemcpyAsync(yhat_out, ctx->yhat, sizeof(float) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     });
@@ -1310,6 +1336,7 @@ int gsrc_forward_backward(gsrc_ctx* ctx, double* loss_out) {
         CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += static_cast<uint64_t>(ctx->cfg.layers) * (ctx->work_layer_fwd() + ctx->work_layer_bwd());
         ctx->timing = phase_timing(ctx, false);
         if (loss_out) *loss_out = *ctx->loss_host;
     });
@@ -1348,6 +1375,7 @@ int gsrc_train_step(gsrc_ctx* ctx, const gsrc_optim_cfg* opt, double* loss_out) 
         CK(cudaMemcpyAsync(ctx->loss_host, ctx->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += static_cast<uint64_t>(ctx->cfg.layers) * (ctx->work_layer_fwd() + ctx->work_layer_bwd());
         ctx->timing = phase_timing(ctx, true);
         if (loss_out) *loss_out = *ctx->loss_host;
     });
@@ -1420,6 +1448,13 @@ int gsrc_high_water_reset(gsrc_ctx* ctx) {
 }
 
 int gsrc_kernel_launches(gsrc_ctx* ctx, int64_t* out) { return guarded(ctx, [&] { *out = ctx->launches; }); }
+int gsrc_work_counter(gsrc_ctx* ctx, uint64_t* scalar_mul_adds, uint64_t* rows_touched) {
+    return guarded(ctx, [&] {
+        if (scalar_mul_adds) *scalar_mul_adds = ctx->work_ma;
+        if (rows_touched) *rows_touched = ctx->work_rows;
+    });
+}
+int gsrc_work_reset(gsrc_ctx* ctx) { return guarded(ctx, [&] { ctx->work_ma = ctx->work_rows = 0; }); }
 
 int gsrc_layer_forward(gsrc_ctx* ctx, int layer) {
     return guarded(ctx, [&] {
@@ -1427,6 +1462,7 @@ int gsrc_layer_forward(gsrc_ctx* ctx, int layer) {
         if (layer < 0 || layer >= ctx->cfg.layers) cfg_err("layer out of range");
         ctx->layer_forward(layer);
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += ctx->work_layer_fwd();
     });
 }
 int gsrc_layer_inverse(gsrc_ctx* ctx, int layer) {
@@ -1436,6 +1472,7 @@ int gsrc_layer_inverse(gsrc_ctx* ctx, int layer) {
         if (ctx->cfg.mode == GSRC_MODE_ALG12) cfg_err("Alg. 1 layers are not invertible (use GSRC or REV)");
         ctx->rev_layer_inverse(layer);
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += ctx->work_layer_fwd();  // the inverse re-applies every block
     });
 }
 int gsrc_layer_backward(gsrc_ctx* ctx, int layer) {
@@ -1444,6 +1481,7 @@ int gsrc_layer_backward(gsrc_ctx* ctx, int layer) {
         if (layer < 0 || layer >= ctx->cfg.layers) cfg_err("layer out of range");
         ctx->layer_backward(layer);
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += ctx->work_layer_bwd();
     });
 }
 
@@ -1486,6 +1524,8 @@ int gsrc_op_spmm(gsrc_ctx* ctx, int transpose, int cols, const float* x, float* 
         ctx->run_tile(a);
         CK(cudaMemcpy2DAsync(y, cols * 4, dy.p, ld * 4, cols * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += static_cast<uint64_t>(ctx->e) * cols;
+        ctx->work_rows += static_cast<uint64_t>(n);
     });
 }
 
@@ -1505,6 +1545,8 @@ int gsrc_op_spmm_sparse(gsrc_ctx* ctx, int transpose, int w, int k, const float*
         ctx->run_tile(a);
         CK(cudaMemcpy2DAsync(y, w * 4, dy.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        ctx->work_ma += static_cast<uint64_t>(ctx->e) * k;
+        ctx->work_rows += static_cast<uint64_t>(n);
     });
 }
 
@@ -1546,6 +1588,7 @@ int gsrc_op_block_forward(gsrc_ctx* ctx, int w, int k, const float* vals, const 
         CK(cudaMemcpy2DAsync(out, w * 4, dout.p, ld * 4, w * 4, n, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         if (gs_k > 0) download_records(dgs.as<uint8_t>(), n, gs_k, gs_vals, gs_idx, ctx->stream);
+        ctx->work_ma += ctx->work_block_fwd(w, k, use_weight != 0);
     });
 }
 
@@ -1611,6 +1654,7 @@ int gsrc_op_block_backward(gsrc_ctx* ctx, int w, int k, const float* m, const in
         CK(cudaStreamSynchronize(ctx->stream));
         if (dW) for (size_t i = 0; i < static_cast<size_t>(w) * w; ++i) dW[i] = use_weight ? g[i] : 0.f;
         if (db) for (int j = 0; j < w; ++j) db[j] = use_bias ? g[static_cast<size_t>(w) * w + j] : 0.f;
+        ctx->work_ma += ctx->work_block_bwd(w, k, use_weight != 0);
     });
 }
 
