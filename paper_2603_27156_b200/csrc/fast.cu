@@ -352,7 +352,7 @@ __device__ __forceinline__ uint32_t gs_key(float v, int col, int w) {
     return col < w ? (__float_as_uint(v) & 0x7fffffffu) + 1u : 0u;
 }
 
-template <int W, bool FULLW, int K = 0>
+template <int W, bool FULLW, int K = 0, bool FM = false>
 __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k_rt, uint8_t* rec_out) {
     const int k = K ? K : k_rt;  // K: k at compile time (0: any k ≤ 16)
     constexpr int G = 16;
@@ -404,7 +404,7 @@ __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k
     if (k == G) {  // last level: the top G as a set; T is its minimum
         merge(0, W / 2, false);
 #pragma unroll
-        for (int i = 0; i < G; ++i) T = min(T, s[i]);
+        for (int i = 0; i < G; i += 2) T = __vimin3_u32(T, s[i], s[i + 1]);  // VIMNMX3
     } else {
         merge(0, W / 2, true);
 #pragma unroll
@@ -415,23 +415,44 @@ __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k
     uint32_t ge[NWD];
 #pragma unroll
     for (int q = 0; q < NWD; ++q) ge[q] = 0u;
+    if constexpr (FULLW && FM) {
+        // "not |v| < T" (one unordered float compare, |.| an operand modifier) is
+        // exactly the key compare while T is a number: a NaN's key exceeds every
+        // number's, and the unordered compare counts it as ≥ T. (T itself a NaN:
+        // the mask is recomputed from the keys on the tie path below.)
+        const float Tf = __uint_as_float(T);
 #pragma unroll
-    for (int c = 0; c < W; c += 4) {
-        const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
-        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        for (int c = 0; c < W; c += 4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ge[(c + q) >> 5] |= static_cast<uint32_t>(gs_key<W, FULLW>(vv[q], c + q, w) >= T) << ((c + q) & 31);
+            for (int q = 0; q < 4; ++q)
+                if (!(fabsf(vv[q]) < Tf)) ge[(c + q) >> 5] |= 1u << ((c + q) & 31);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < W; c += 4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(Ts + zo(r, c));
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ge[(c + q) >> 5] |= static_cast<uint32_t>(gs_key<W, FULLW>(vv[q], c + q, w) >= T) << ((c + q) & 31);
+        }
     }
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < NWD; ++q) cnt += __popc(ge[q]);
-    if (cnt != k) {  // ties at T beyond k: keep keys > T, then the lowest-column ties
+    const bool t_nan = FULLW && FM && T > 0x7f800000u;
+    if (cnt != k || t_nan) {  // ties at T beyond k: keep keys > T, then the lowest-column ties
         uint32_t gt[NWD];
 #pragma unroll
         for (int q = 0; q < NWD; ++q) gt[q] = 0u;
+        if (t_nan)
+#pragma unroll
+            for (int q = 0; q < NWD; ++q) ge[q] = 0u;
         for (int c = 0; c < W; ++c) {
-            const float v = Ts[zo(r, c)];
-            gt[c >> 5] |= static_cast<uint32_t>(gs_key<W, FULLW>(v, c, w) > T) << (c & 31);
+            const uint32_t key = gs_key<W, FULLW>(Ts[zo(r, c)], c, w);
+            gt[c >> 5] |= static_cast<uint32_t>(key > T) << (c & 31);
+            if (t_nan) ge[c >> 5] |= static_cast<uint32_t>(key >= T) << (c & 31);
         }
         int take = k;
 #pragma unroll
@@ -477,10 +498,12 @@ __device__ __forceinline__ void gs_row_impl(const float* Ts, int r, int w, int k
         if (q < nv4) reinterpret_cast<float4*>(rec_out + 16)[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
 }
 
-template <int W, int G, int K = 0>
+// FM: the selection mask by unordered float compares (fewer instructions; used
+// where the GS epilogue bounds the kernel, k_fws)
+template <int W, int G, int K = 0, bool FM = false>
 __device__ __forceinline__ void gs_row(const float* Ts, int r, int w, int k, uint8_t* rec_out) {
     static_assert(G == 16, "top-16 tree (k ≤ 16)");
-    if (K && k == K && w == W) gs_row_impl<W, true, K>(Ts, r, w, k, rec_out);
+    if (K && k == K && w == W) gs_row_impl<W, true, K, FM>(Ts, r, w, k, rec_out);
     else if (w == W) gs_row_impl<W, true>(Ts, r, w, k, rec_out);
     else gs_row_impl<W, false>(Ts, r, w, k, rec_out);
 }
@@ -857,7 +880,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
                 for (int c = 0; c < W; c += 32) tma_store_2d(&a.tm_x, Ob + (c >> 5) * (TR * 32), c, row0);
                 tma_store_commit();
             }
-            if (a.gs_out && valid) gs_row<W, 16, KS == 16 ? 16 : 0>(Ob, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
+            if (a.gs_out && valid) gs_row<W, 16, KS == 16 ? 16 : 0, true>(Ob, t, a.w, a.k_gs, a.gs_out + static_cast<size_t>(row) * rec_bytes(a.k_gs));
             named_bar_sync(2, TR);  // every read of Out is done
             if (t == 0) {
                 tma_store_wait_read();
