@@ -1,5 +1,6 @@
 #!/bin/bash
-# Quick check: fast-path GPU tests, c3 bench, and per-launch metrics of the main kernels.
+# Quick check: fast-path GPU tests, c3 bench, and per-launch metrics of the kernels matching a regex.
+# Usage: bash tools/gpu_check.sh <kernel-regex> <skip> <count>
 set -u
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_fast.py tests/test_gpu_config_parity.py -m gpu -q -x > gpurun_out/pytest_fast.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_fast.log

@@ -1,5 +1,5 @@
 #!/bin/bash
-# ncu --set full (with source) of one kernel on the c3 bench step. Usage: bash tools/gpu_prof1.sh <regex> <skip> <count> <out>
+# ncu --set full (with source) of one kernel on the c3 bench step. Usage: bash tools/gpu_ncu_kernel.sh <regex> <skip> <count> <out>
 set -u
 mkdir -p gpurun_out
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$1" -s $2 -c $3 -f -o gpurun_out/$4 \
