@@ -961,13 +961,19 @@ __global__ void __launch_bounds__(TPR * TR, 2) k_bin2(const __grid_constant__ Fa
             dw_pending = false;
         }
         const int tnext = tile_i + static_cast<int>(gridDim.x);
-        if (tid == 0) {  // the next tile's slots and mask records
+        if (tid == 0) {  // the next tile's slots, mask records and its own rows of G_i (± a halo)
             prefetch_tile_meta(a.dir, tnext, n_tiles, a.n);
             if (tnext < n_tiles) {
                 const void* p;
                 uint32_t b;
                 mask_span(tnext, p, b);
                 prefetch_l2_bulk(p, b);
+                // most of a circuit row's neighbours are the rows next to it: their
+                // G rows toward L2 now, so the next tile's gather passes hit L2
+                constexpr int kH = 8;
+                const int lo = tnext * TR - kH > 0 ? tnext * TR - kH : 0;
+                const int hi = tnext * TR + TR + kH < a.n ? tnext * TR + TR + kH : a.n;
+                prefetch_l2_bulk(a.x_in + static_cast<size_t>(lo) * a.ld, static_cast<uint32_t>(hi - lo) * static_cast<uint32_t>(a.ld) * 4u);
             }
         }
         uint32_t hm = 0u;  // this thread's mask columns (mask of a padding / invalid row: empty)
