@@ -723,11 +723,16 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
     constexpr uint32_t TCOLS = 2 * W < 32 ? 32 : 2 * W;  // two accumulators
     const int RB = rec_bytes(KS ? KS : a.k);
 
-    for (int i = tid; i < W * W; i += 2 * TR) {  // transform operand Bᵀ[n][m] (K-major SW128)
+    // transform operand Bᵀ[n][m] (K-major SW128). On the residual grid it holds
+    // tf32(W)·2^s: the tensor core reads tf32(W) unchanged, and every product and
+    // partial sum scales by the power of two exactly, so the accumulator holds
+    // h·2^s and the epilogue's rounding (dev::quant) needs no multiply in
+    const bool grid = a.qs != 0.f;
+    for (int i = tid; i < W * W; i += 2 * TR) {
         const int r = i / W, c = i % W;
         float v = 0.f;
         if (r < a.w && c < a.w) v = a.gemm_t ? a.Wm[c * a.w + r] : a.Wm[r * a.w + c];
-        Ws[tile::boff<W>(c, r)] = v;
+        Ws[tile::boff<W>(c, r)] = grid ? __fmul_rn(tile::tf32_op(v), a.qs) : v;
     }
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) { mbar_init(&bar[b], 1); mbar_init(&bar[2 + b], TR); mbar_init(&bar[4 + b], 1); }
@@ -854,16 +859,21 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
             for (int c0 = 0; c0 < W; c0 += 16) {
                 float h[16];
                 tmem_ld<16>(tmem + tlane + static_cast<uint32_t>(b * W + c0), h);
+                if (a.bias) {  // (scaled with the accumulator on the grid: (h + b)·2^s exactly)
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const float bv = c0 + q < a.w ? __ldg(a.bias + c0 + q) : 0.f;
+                        h[q] = __fadd_rn(h[q], grid ? __fmul_rn(bv, a.qs) : bv);
+                    }
+                }
+                if (grid) {  // dev::quant(h + b): rint((h + b)·2^s)·2^-s
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) h[q] = __fmul_rn(rintf(h[q]), a.qi);
+                }
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) {
                     const int c = c0 + q;
-                    float o[4];
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        float hv = h[q + jj];
-                        if (a.bias) hv = __fadd_rn(hv, c + jj < a.w ? __ldg(a.bias + c + jj) : 0.f);
-                        o[jj] = dev::quant(hv, a.qs, a.qi);
-                    }
+                    float o[4] = {h[q], h[q + 1], h[q + 2], h[q + 3]};
                     float4* rp = reinterpret_cast<float4*>(Ob + zo(t, c));
                     const float4 R = *rp;
                     if (KIND == FWD) { o[0] = __fadd_rn(R.x, o[0]); o[1] = __fadd_rn(R.y, o[1]); o[2] = __fadd_rn(R.z, o[2]); o[3] = __fadd_rn(R.w, o[3]); }
