@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(2 * TR, 2) k_fws(const __grid_constant__ FastA
             const int tile_i = tile_of(j);
             const int row0 = tile_i * TR, row = row0 + t;
             const int b = j & 1;
-            if (KIND == INV && j == my_tiles - 1) dev::pdl_trigger();
+            // no early pdl_trigger: with it, the successor's CTAs crowd this grid's tail (measured)
             if (t == 0) {
                 prefetch_tile_meta(a.dir, tile_i + 2 * static_cast<int>(gridDim.x), n_tiles, a.n);
                 if (j + 1 < my_tiles) {  // Win[(j + 1) & 1] was last read by tile j − 1 (before its barriers)
