@@ -1243,6 +1243,7 @@ __global__ void __launch_bounds__(kHubChunk) k_hub_rows(FastArgs a, const int4* 
     float* acc = slot;
     const int tid = threadIdx.x;
     dev::pdl_wait();
+    dev::pdl_trigger();  // the block kernel that follows may start its on-chip prologue while the hub rows finish
     // work item: {row, first edge, end edge, first segment of the chunk}, {hub index, row's first partial}
     const int4 ia = __ldg(items + 2 * blockIdx.x), ib = __ldg(items + 2 * blockIdx.x + 1);
     const int r = ia.x, e0 = ia.y, e1 = ia.z, c0 = ia.w, h = ib.x;
